@@ -1,0 +1,402 @@
+"""B200-native VMonarch attention forward (arXiv 2601.22275).
+
+Python mirror of the reference operator API (/root/reference/proj/include/vmonarch/video.hpp,
+monarch.hpp, flash_entropy.hpp) on top of the C ABI in include/vmb.h (libvmb.so, hand-written
+sm_100a kernels).  Tensors are torch CUDA tensors (torch is the device-memory/stream plumbing);
+every compute call goes through libvmb.so.  There is no CPU fallback: if the extension is
+missing, importing this package raises.
+
+Reference -> here
+  TokenGrid / VMonarchConfig (video.hpp:16-36)          TokenGrid / VMonarchConfig
+  vmonarch_attention<T> (video.hpp:84-150)              vmonarch_attention
+  r_update / l_update (monarch.hpp:53-147)              r_update / l_update
+  flash_entropy_fwd (flash_entropy.hpp:85-139)          flash_entropy_fwd
+  dense_forward (oracle.hpp:36-72)                      dense_forward
+  factorize / flops_estimate (video.cpp:13-59)          factorize / flops_estimate
+  make_perm (perm.hpp:19-30)                            make_perm
+  std::invalid_argument / domain_error / logic_error    DimensionError / DomainError / StateError
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence, Tuple
+
+import torch
+
+__all__ = [
+    "TokenGrid", "VMonarchConfig", "CostReport", "DimensionError", "DomainError", "StateError",
+    "vmonarch_attention", "r_update", "l_update", "flash_entropy_fwd", "dense_forward",
+    "factorize", "flops_estimate", "make_perm", "preset_grid", "export_factors", "lib",
+    "kernel_launch_count", "LIB_PATH",
+]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libvmb.so")
+
+
+class DimensionError(ValueError):
+    """std::invalid_argument("dimension error: ...") in the reference (check.hpp:10-12)."""
+
+
+class DomainError(ArithmeticError):
+    """std::domain_error("domain error: ...") in the reference (check.hpp:14-16)."""
+
+
+class StateError(RuntimeError):
+    """std::logic_error("state error: ...") in the reference (check.hpp:18-20)."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is not built; run `python __graft_entry__.py build` (make -C "
+            "paper_2601_22275_b200/csrc).  There is no CPU fallback.")
+    return C.CDLL(LIB_PATH)
+
+
+lib = _load()
+
+_P, _I64, _I32, _D, _F = C.c_void_p, C.c_int64, C.c_int32, C.c_double, C.c_float
+
+
+class _Grid(C.Structure):
+    _fields_ = [("t_frames", _I64), ("h", _I64), ("w", _I64), ("head_dim", _I64), ("heads", _I64),
+                ("batch", _I64)]
+
+
+class _Cfg(C.Structure):
+    _fields_ = [("iters", _I64), ("clamp_min", _D), ("clamp_enabled", _I32),
+                ("recompute_first_frame", _I32), ("override_m", _I64), ("override_b", _I64),
+                ("tile_br", _I64), ("tile_bc", _I64)]
+
+
+class _Strides(C.Structure):
+    _fields_ = [("batch", _I64), ("head", _I64), ("token", _I64)]
+
+
+def _sig(name, args, res=C.c_int):
+    f = getattr(lib, name)
+    f.argtypes = args
+    f.restype = res
+    return f
+
+
+_vmb_last_error = _sig("vmb_last_error", [], C.c_char_p)
+_vmb_factorize = _sig("vmb_factorize", [C.POINTER(_Grid), C.POINTER(_Cfg), C.POINTER(_I64), C.POINTER(_I64)])
+_vmb_make_perm = _sig("vmb_make_perm", [_I64, _I64, _P])
+_vmb_flops = _sig("vmb_flops_estimate", [C.POINTER(_Grid), C.POINTER(_Cfg), _I64] + [_P] * 6)
+_vmb_ws_size = _sig("vmb_workspace_size", [C.POINTER(_Grid), C.POINTER(_Cfg), C.c_int], C.c_size_t)
+_vmb_fwd = _sig("vmb_vmonarch_fwd", [C.POINTER(_Grid), C.POINTER(_Cfg), C.c_int, _P, _P, _P, _P,
+                                     C.POINTER(_Strides), C.POINTER(_Strides), _P, C.c_size_t, _P])
+_vmb_ws_status = _sig("vmb_workspace_status", [_P, _P])
+_vmb_export = _sig("vmb_export_factors", [C.POINTER(_Grid), C.POINTER(_Cfg), C.c_int, _P, _P,
+                                          C.POINTER(_Strides), _P, _P, _P, _P])
+_vmb_rstep = _sig("vmb_rstep", [_I64, _I64, _I64, _I64, C.c_int, _P, _P, _P, _D, _I32, _P, _P, _P, _P])
+_vmb_lstep = _sig("vmb_lstep", [_I64, _I64, _I64, _I64, C.c_int, _P, _P, _P, _P, _P, _P, _P])
+_vmb_flash = _sig("vmb_flash_entropy_fwd", [_I64, _I64, _I64, _I64, C.c_int, _P, _P, _P, _F, _P, _P, _P, _P])
+_vmb_dense = _sig("vmb_dense_fwd", [_I64, _I64, _I64, C.c_int, _P, _P, _P, _P, _P])
+_vmb_launches = _sig("vmb_kernel_launch_count", [], C.c_uint64)
+_vmb_selftest = _sig("vmb_selftest_umma", [_I32, _P, _P, _P, _P])
+
+VMB_F32, VMB_BF16 = 0, 1
+_ERRORS = {1: DimensionError, 2: DomainError, 3: StateError, 4: CudaError, 5: CudaError}
+
+
+def _check(status: int):
+    if status != 0:
+        msg = (_vmb_last_error() or b"").decode()
+        raise _ERRORS.get(status, CudaError)(msg)
+
+
+def kernel_launch_count() -> int:
+    """Kernels libvmb.so has launched in this process (all entry points)."""
+    return int(_vmb_launches())
+
+
+# ----------------------------------------------------------------------------- config types
+@dataclass
+class TokenGrid:
+    """video.hpp:16-27.  Frame-major tokens: token = t*(h*w) + r*w + c."""
+    t_frames: int = 1
+    h: int = 1
+    w: int = 1
+    head_dim: int = 64
+    heads: int = 1
+    batch: int = 1
+
+    def tokens(self) -> int:
+        return self.t_frames * self.h * self.w
+
+    def frame_tokens(self) -> int:
+        return self.h * self.w
+
+    def units(self) -> int:
+        return self.heads * self.batch
+
+    def _c(self) -> _Grid:
+        return _Grid(self.t_frames, self.h, self.w, self.head_dim, self.heads, self.batch)
+
+
+@dataclass
+class VMonarchConfig:
+    """video.hpp:29-36 (+ TileConfig flash_entropy.hpp:13-16, accepted for API parity)."""
+    iters: int = 2
+    clamp_min: float = 0.1
+    clamp_enabled: bool = True
+    recompute_first_frame: bool = True
+    override_m_b: Optional[Tuple[int, int]] = None
+    tiles: Tuple[int, int] = (64, 64)
+
+    def _c(self) -> _Cfg:
+        om, ob = self.override_m_b if self.override_m_b else (0, 0)
+        return _Cfg(self.iters, self.clamp_min, int(self.clamp_enabled), int(self.recompute_first_frame),
+                    om, ob, self.tiles[0], self.tiles[1])
+
+
+@dataclass
+class CostReport:
+    """video.hpp:38-47."""
+    sparsity: float = 0.0
+    sparsity_approx: float = 0.0
+    monarch_flops: int = 0
+    full_attn_flops: int = 0
+    recompute_flops: int = 0
+    reduction_ratio: float = 0.0
+
+
+_PRESETS = {"wan-61f": (16, 28, 52), "wan-141f": (36, 28, 52), "wan-321f": (81, 28, 52)}
+
+
+def preset_grid(name: str) -> Optional[Tuple[int, int, int]]:
+    """video.cpp:5-11 preset latent grids (T, h, w)."""
+    return _PRESETS.get(name)
+
+
+def factorize(grid: TokenGrid, cfg: VMonarchConfig = VMonarchConfig()) -> Tuple[int, int]:
+    """video.cpp:13-22: (m, b) = (T, h*w) unless overridden with m*b = N."""
+    m, b = _I64(), _I64()
+    g, c = grid._c(), cfg._c()
+    _check(_vmb_factorize(C.byref(g), C.byref(c), C.byref(m), C.byref(b)))
+    return m.value, b.value
+
+
+def flops_estimate(grid: TokenGrid, cfg: VMonarchConfig, d: int) -> CostReport:
+    """video.cpp:36-59 — the FLOP convention of the headline metric (2 FLOPs/MAC, matmuls)."""
+    vals = [C.c_double(), C.c_double(), C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_double()]
+    g, c = grid._c(), cfg._c()
+    _check(_vmb_flops(C.byref(g), C.byref(c), d, *[C.addressof(x) for x in vals]))
+    return CostReport(vals[0].value, vals[1].value, vals[2].value, vals[3].value, vals[4].value,
+                      vals[5].value)
+
+
+def make_perm(b: int, n: int) -> list:
+    """perm.hpp:19-30 forward_index (bit-exact)."""
+    out = (C.c_int64 * max(n, 1))()
+    _check(_vmb_make_perm(b, n, C.addressof(out)))
+    return list(out)[:n]
+
+
+# ----------------------------------------------------------------------------- helpers
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return VMB_F32
+    if t.dtype == torch.bfloat16:
+        return VMB_BF16
+    raise DimensionError(f"dimension error: unsupported dtype {t.dtype} (float32 or bfloat16)")
+
+
+def _stream() -> C.c_void_p:
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise DimensionError("dimension error: tensors must be CUDA tensors (no CPU path)")
+
+
+def _bhsd_strides(t: torch.Tensor, grid: TokenGrid) -> _Strides:
+    """Accept (units, N, d), (B, H, N, d) or BSHD (B, N, H, d) given as a (B, H, N, d) view."""
+    n, d = grid.tokens(), grid.head_dim
+    if t.dim() == 3:
+        if tuple(t.shape) != (grid.units(), n, d):
+            raise DimensionError("dimension error: expected one Q/K/V matrix per batch*head unit "
+                                 f"of shape ({grid.units()}, {n}, {d}), got {tuple(t.shape)}")
+        if t.stride(2) != 1:
+            raise DimensionError("dimension error: head dim must be contiguous")
+        su = t.stride(0)
+        return _Strides(su * grid.heads, su, t.stride(1))
+    if t.dim() == 4:
+        if tuple(t.shape) != (grid.batch, grid.heads, n, d):
+            raise DimensionError(f"dimension error: expected (B, H, N, d) = ({grid.batch}, {grid.heads}, "
+                                 f"{n}, {d}), got {tuple(t.shape)}")
+        if t.stride(3) != 1:
+            raise DimensionError("dimension error: head dim must be contiguous")
+        return _Strides(t.stride(0), t.stride(1), t.stride(2))
+    raise DimensionError("dimension error: Q/K/V must be 3-D (units, N, d) or 4-D (B, H, N, d)")
+
+
+_WS_CACHE: dict = {}
+
+
+def _workspace(grid: TokenGrid, cfg: VMonarchConfig, dt: int, device) -> torch.Tensor:
+    g, c = grid._c(), cfg._c()
+    nbytes = int(_vmb_ws_size(C.byref(g), C.byref(c), dt))
+    if nbytes == 0:
+        _check(1)
+    key = (device, nbytes)
+    ws = _WS_CACHE.get(key)
+    if ws is None:
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        _WS_CACHE.clear()
+        _WS_CACHE[key] = ws
+    return ws
+
+
+# ----------------------------------------------------------------------------- the operator
+def vmonarch_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, grid: TokenGrid,
+                       cfg: VMonarchConfig = VMonarchConfig(), out: Optional[torch.Tensor] = None,
+                       factors_out: Optional[list] = None, check: bool = True) -> torch.Tensor:
+    """video.hpp:84-150 on the GPU.
+
+    q, k, v: CUDA tensors (units, N, d) [unit u = b*H + h], or (B, H, N, d) views (BSHD
+    activations pass as ``x.transpose(1, 2)``), float32 (parity mode) or bfloat16.
+    Returns O with the layout of ``q`` (3-D) or a (B, H, N, d) tensor.
+    ``factors_out``: if a list, receives per-unit (L (b,m,m), R (m,b,b)) fp32 tensors (small N).
+    ``check``: synchronise and raise DomainError for device-detected domain errors
+    (non-finite Q, monarch.hpp:44).  Set False inside timed loops.
+    """
+    _require_cuda(q, k, v, out)
+    dt = _dtype_code(q)
+    if k.dtype != q.dtype or v.dtype != q.dtype:
+        raise DimensionError("dimension error: Q, K, V must share dtype")
+    sq, sk, sv = _bhsd_strides(q, grid), _bhsd_strides(k, grid), _bhsd_strides(v, grid)
+    if (sk.batch, sk.head, sk.token) != (sq.batch, sq.head, sq.token) or \
+            (sv.batch, sv.head, sv.token) != (sq.batch, sq.head, sq.token):
+        # the ABI takes one stride set for Q/K/V; normalise the odd ones out
+        k = k.contiguous() if (sk.batch, sk.head, sk.token) != (sq.batch, sq.head, sq.token) else k
+        v = v.contiguous() if (sv.batch, sv.head, sv.token) != (sq.batch, sq.head, sq.token) else v
+        if not (q.is_contiguous() and k.is_contiguous() and v.is_contiguous()):
+            q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+        sq = _bhsd_strides(q, grid)
+    if out is None:
+        out = torch.empty(q.shape, dtype=q.dtype, device=q.device)
+    so = _bhsd_strides(out, grid)
+    ws = _workspace(grid, cfg, dt, q.device)
+    g, c = grid._c(), cfg._c()
+    st = _stream()
+    _check(_vmb_fwd(C.byref(g), C.byref(c), dt, _ptr(q), _ptr(k), _ptr(v), _ptr(out), C.byref(sq),
+                    C.byref(so), _ptr(ws), ws.numel(), st))
+    if check or factors_out is not None:
+        _check(_vmb_ws_status(_ptr(ws), st))
+    if factors_out is not None:
+        m, b = factorize(grid, cfg)
+        U = grid.units()
+        L = torch.empty((U, b, m, m), dtype=torch.float32, device=q.device)
+        R = torch.empty((U, m, b, b), dtype=torch.float32, device=q.device)
+        _check(_vmb_export(C.byref(g), C.byref(c), dt, _ptr(q), _ptr(k), C.byref(sq), _ptr(ws), _ptr(L),
+                           _ptr(R), st))
+        factors_out.clear()
+        factors_out.extend((L[u], R[u]) for u in range(U))
+    return out
+
+
+def export_factors(q, k, grid, cfg, dtype_code):
+    """Factor export for the last vmonarch_attention call on this device (MonarchFactors)."""
+    m, b = factorize(grid, cfg)
+    U = grid.units()
+    L = torch.empty((U, b, m, m), dtype=torch.float32, device=q.device)
+    R = torch.empty((U, m, b, b), dtype=torch.float32, device=q.device)
+    ws = _workspace(grid, cfg, dtype_code, q.device)
+    g, c = grid._c(), cfg._c()
+    sq = _bhsd_strides(q, grid)
+    _check(_vmb_export(C.byref(g), C.byref(c), dtype_code, _ptr(q), _ptr(k), C.byref(sq), _ptr(ws),
+                       _ptr(L), _ptr(R), _stream()))
+    return L, R
+
+
+# ----------------------------------------------------------------------------- half steps
+def r_update(aR: torch.Tensor, cR: torch.Tensor, Kb: torch.Tensor, clamp_min: float = 0.1,
+             clamp_enabled: bool = True, want_R: bool = False):
+    """monarch.hpp:53-103 for (units, m, b, d) state.  Returns (aL (units,b,m,d), cL (units,b,m) f32, R)."""
+    _require_cuda(aR, cR, Kb)
+    U, m, b, d = aR.shape
+    dt = _dtype_code(aR)
+    aR, Kb = aR.contiguous(), Kb.contiguous().to(aR.dtype)
+    cR = cR.contiguous().float()
+    aL = torch.empty((U, b, m, d), dtype=aR.dtype, device=aR.device)
+    cL = torch.empty((U, b, m), dtype=torch.float32, device=aR.device)
+    R = torch.empty((U, m, b, b), dtype=torch.float32, device=aR.device) if want_R else None
+    _check(_vmb_rstep(U, m, b, d, dt, _ptr(aR), _ptr(cR), _ptr(Kb), clamp_min, int(clamp_enabled), _ptr(aL),
+                      _ptr(cL), _ptr(R), _stream()))
+    return aL, cL, R
+
+
+def l_update(Qb: torch.Tensor, aL: torch.Tensor, cL: torch.Tensor, want_L: bool = False):
+    """monarch.hpp:105-147 for (units, b, m, d) state.  Returns (aR (units,m,b,d), cR (units,m,b) f32, L)."""
+    _require_cuda(Qb, aL, cL)
+    U, b, m, d = Qb.shape
+    dt = _dtype_code(Qb)
+    Qb, aL, cL = Qb.contiguous(), aL.contiguous().to(Qb.dtype), cL.contiguous().float()
+    aR = torch.empty((U, m, b, d), dtype=Qb.dtype, device=Qb.device)
+    cR = torch.empty((U, m, b), dtype=torch.float32, device=Qb.device)
+    L = torch.empty((U, b, m, m), dtype=torch.float32, device=Qb.device) if want_L else None
+    _check(_vmb_lstep(U, m, b, d, dt, _ptr(Qb), _ptr(aL), _ptr(cL), _ptr(aR), _ptr(cR), _ptr(L), _stream()))
+    return aR, cR, L
+
+
+# ----------------------------------------------------------------------------- attention kernels
+def flash_entropy_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, q_scale: float = 1.0,
+                      want_entropy: bool = True):
+    """flash_entropy.hpp:85-139: (out, lse, entropy) for (units, nq, d) / (units, nk, d) inputs.
+    Q must carry its scale (q_scale multiplies the logits; 1.0 = reference semantics)."""
+    _require_cuda(q, k, v)
+    squeeze = q.dim() == 2
+    if squeeze:
+        q, k, v = q[None], k[None], v[None]
+    U, nq, d = q.shape
+    nk = k.shape[1]
+    if k.shape[2] != d or v.shape[2] != d:
+        raise DimensionError("dimension error: Q, K, V must share head dim")
+    if v.shape[1] != nk:
+        raise DimensionError("dimension error: K and V must share row count")
+    if nk < 1:
+        raise DomainError("domain error: attention over empty keys")
+    dt = _dtype_code(q)
+    q, k, v = q.contiguous(), k.contiguous().to(q.dtype), v.contiguous().to(q.dtype)
+    o = torch.empty_like(q)
+    lse = torch.empty((U, nq), dtype=torch.float32, device=q.device)
+    ent = torch.empty((U, nq), dtype=torch.float32, device=q.device) if want_entropy else None
+    _check(_vmb_flash(U, nq, nk, d, dt, _ptr(q), _ptr(k), _ptr(v), q_scale, _ptr(o), _ptr(lse), _ptr(ent),
+                      _stream()))
+    if squeeze:
+        return o[0], lse[0], (ent[0] if ent is not None else None)
+    return o, lse, ent
+
+
+def dense_forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor) -> torch.Tensor:
+    """oracle.hpp:36-72 semantics (softmax(Q K^T / sqrt d) V) on the tcgen05 attention kernel."""
+    _require_cuda(q, k, v)
+    U, n, d = q.shape
+    dt = _dtype_code(q)
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    o = torch.empty_like(q)
+    _check(_vmb_dense(U, n, d, dt, _ptr(q), _ptr(k), _ptr(v), _ptr(o), _stream()))
+    return o
+
+
+def selftest_umma(mode: int, A: torch.Tensor, B: torch.Tensor) -> torch.Tensor:
+    """tcgen05/TMA building-block check (see csrc/kernels/selftest.cu)."""
+    C_ = torch.empty((128, 128), dtype=torch.float32, device=A.device)
+    _check(_vmb_selftest(mode, _ptr(A.contiguous()), _ptr(B.contiguous()), _ptr(C_), _stream()))
+    return C_

@@ -1,0 +1,155 @@
+// internal.hpp — host-side declarations shared by the libvmb translation units.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#include <atomic>
+#include <cstdint>
+#include <string>
+
+#include "../../include/vmb.h"
+
+namespace vmb {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+struct Error {
+    vmb_status status;
+    std::string msg;
+};
+#define VMB_CHECK_CUDA(expr)                                                                    \
+    do {                                                                                        \
+        cudaError_t e__ = (expr);                                                               \
+        if (e__ != cudaSuccess)                                                                 \
+            throw ::vmb::Error{VMB_ERR_CUDA, std::string("cuda error: ") + #expr + ": " +       \
+                                                 cudaGetErrorString(e__)};                      \
+    } while (0)
+#define VMB_REQUIRE_DIM(cond, msg)                                                              \
+    do {                                                                                        \
+        if (!(cond)) throw ::vmb::Error{VMB_ERR_DIM, std::string("dimension error: ") + (msg)}; \
+    } while (0)
+#define VMB_REQUIRE_DOMAIN(cond, msg)                                                           \
+    do {                                                                                        \
+        if (!(cond)) throw ::vmb::Error{VMB_ERR_DOMAIN, std::string("domain error: ") + (msg)}; \
+    } while (0)
+
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+// Throws on a launch error of the kernel just enqueued.
+void check_launch(const char* what);
+
+// ---------------------------------------------------------------- views
+// Row (u, a, c) of a [batch, head, a, c, d] view lives at element offset
+//   (u / H) * sB + (u % H) * sH + a * sa + c * sc,  d contiguous.
+struct View {
+    const void* base = nullptr;
+    int64_t sB = 0, sH = 0, sa = 0, sc = 0;
+    int32_t H = 1;
+};
+
+// Device status word (first 16 bytes of every workspace).
+enum : int32_t { kStatusOk = 0, kStatusNonFiniteQ = 1, kStatusClampDomain = 2 };
+
+// ---------------------------------------------------------------- TMA maps
+// bf16 5-D tiled map over `base` with dims (innermost first) and byte strides of
+// dims 1..4; 128B swizzle, zero OOB fill.
+CUtensorMap make_tmap_bf16_5d(const void* base, const uint64_t dims[5],
+                              const uint64_t strides_bytes[4], const uint32_t box[5]);
+bool tmap_supported();
+
+// ---------------------------------------------------------------- SIMT kernels (any dtype)
+struct SimtRstepArgs {
+    View A;            // query rows (u, k, i): aR or Q
+    float qscale;      // multiplies the logits
+    const float* cR;   // (U, m, b) or nullptr (== 1)
+    float clamp_min;
+    int clamp_enabled;
+    View K;            // key rows (u, k, l)
+    View V;            // value rows (u, k, l)
+    View Out;          // output rows (u, k, i)  (aL or y)
+    float* cL;         // (U, b, m) or nullptr
+    float* R;          // (U, m, b, b) or nullptr
+    int64_t U, m, b, d;
+    int32_t* status;
+};
+struct SimtLstepArgs {
+    View Q;            // Qb rows (u, i, j)
+    float qscale;
+    View aL;           // rows (u, i, k)
+    const float* cL;   // (U, b, m)
+    View aR;           // ITER: output rows (u, k, i)
+    float* cR;         // ITER: (U, m, b)
+    View Y;            // FINAL: rows (u, k, i)
+    View O;            // FINAL: output rows (u, j, i)
+    int32_t skip_j0;   // FINAL: rows j == 0 are produced elsewhere (recompute)
+    float* L;          // (U, b, m, m) or nullptr
+    int32_t final_mode;
+    int64_t U, m, b, d;
+};
+struct SimtFlashArgs {
+    View Q;            // rows (u, 0, r), r < nq
+    float qscale;
+    View K, V;         // rows (u, 0, l), l < nk
+    View O;            // rows (u, 0, r)
+    float* lse;        // (U, nq) or nullptr
+    float* ent;        // (U, nq) or nullptr
+    int64_t U, nq, nk, d;
+};
+void simt_rstep(const SimtRstepArgs& a, bool bf16, cudaStream_t s);
+void simt_lstep(const SimtLstepArgs& a, bool bf16, cudaStream_t s);
+void simt_flash(const SimtFlashArgs& a, bool bf16, cudaStream_t s);
+void check_finite_rows(View q, int64_t U, int64_t rows, int64_t d, bool bf16, int32_t* status,
+                       cudaStream_t s);
+void check_clamp_domain(const float* cR, int64_t n, int32_t* status, cudaStream_t s);
+
+// ---------------------------------------------------------------- tcgen05 kernels (bf16, d = 128)
+struct TcFaArgs {
+    // segments: grid.y enumerates (unit, segment); segment s of unit u covers
+    // query rows [q_row0 + s*q_seg_stride, +q_len) and key rows [kv_row0 + s*kv_seg_stride, +kv_len).
+    CUtensorMap tmQ, tmK, tmV;   // 5-D maps: (d, row, seg, head, batch)
+    int32_t nseg;                // segments per unit
+    int32_t q_len, kv_len;       // rows per segment
+    int32_t qH, kH, oHn;         // heads per batch of the q map, the k/v maps, the outputs
+    const float* cR;             // per-row temperature source (U, nseg, q_len) or nullptr
+    float qscale;                // logits multiplier (log2e applied inside)
+    float clamp_min;
+    int32_t clamp_enabled;
+    int32_t nv;                  // 1: O = P*[V]; 2: O = P*[K | V] (V is the 2nd operand)
+    int32_t v_is_k;              // nv == 1 and the value operand is the key tile itself
+    // outputs: row (u, s, r) of operand t at out[t] + (u/H)*oB + (u%H)*oH + s*oS + r*oR
+    void* out0;
+    void* out1;
+    int64_t oB[2], oH[2], oS[2], oR[2];
+    float* cl_out;               // natural-log sum p ln p per row: (u, r, s) at u*q_len*nseg + r*nseg + s
+    float* lse_out;              // (u, s, r) at (u*nseg + s)*q_len + r
+    int32_t* status;             // non-finite detection
+    int32_t check_finite;
+};
+void tc_fa_launch(const TcFaArgs& a, int64_t U, cudaStream_t s);
+
+struct TcLstepArgs {
+    CUtensorMap tmQ;    // Q rows, 5-D (d, i, j, head, batch): Qb[i][j]
+    CUtensorMap tmAL;   // aL rows, 5-D (d, k, i, unit, 1)
+    CUtensorMap tmY;    // y rows, 5-D (d, i, k, unit, 1) (final mode)
+    const float* cL;    // (U, b, m)
+    float qscale;
+    int32_t m, b;
+    int32_t H;          // heads per batch of the Q map
+    int32_t oHn;        // heads per batch of O
+    int32_t final_mode;
+    // ITER outputs
+    __nv_bfloat16* aR;  // (U, m, b, d) contiguous
+    float* cR;          // (U, m, b)
+    float ar_scale;     // multiplies the aR epilogue
+    // FINAL outputs: O row (u, j, i) at O + (u/H)*oB + (u%H)*oH + j*oJ + i*oI
+    __nv_bfloat16* O;
+    int64_t oB, oH, oJ, oI;
+    int32_t skip_j0;
+};
+void tc_lstep_launch(const TcLstepArgs& a, int64_t U, cudaStream_t s);
+
+void selftest_umma(int mode, const void* A, const void* B, float* C, cudaStream_t s);
+
+}  // namespace vmb

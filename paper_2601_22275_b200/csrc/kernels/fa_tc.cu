@@ -1,0 +1,358 @@
+// fa_tc.cu — tcgen05 flash-attention kernel with fused online entropy (bf16, d = 128).
+//
+// One kernel serves three hot-path roles:
+//   * R half-step  (monarch.hpp:53-103): query = aR[k] (or Q on the first step), key = value
+//     = Kb[k], per-row temperature 1/max(cR, clamp) folded into the softmax scale, outputs
+//     aL rows (strided into (b,m,d)) and cL = sum_l R ln R.          <NB=1, NO=1>
+//   * last R half-step with the assembly GEMM y[k] = R[k] Vb[k] fused (monarch.hpp:182-185):
+//     O = P [K | V], outputs aL and y.                                  <NB=2, NO=2>
+//   * first-frame recompute / dense baseline (flash_entropy.hpp:85-139, video.hpp:117-126):
+//     query = Q rows, key/value = all keys, outputs O (+ lse, entropy). <NB=2, NO=1>
+//
+// CTA = one 128-row query tile of one segment.  Warp roles (256 threads):
+//   warp 0      TMA producer: Q tile once, then a ring of KV stages (NB tiles of 128x128)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 4-7   softmax / statistics / epilogue; thread t owns query row t (TMEM lane t)
+// TMEM (512 cols): S0 [0,128), S1 [128,256) double-buffered scores; P (bf16) overwrites
+// the first 64 columns of its S buffer; O accumulators at [256, 256 + 128*NO).
+// S_{j+1} = Q K_{j+1}^T is issued before waiting for P_j, so the tensor pipe computes the
+// next score tile while the softmax warps work on the current one.
+//
+// Statistics are kept in base 2 with a lazily-updated reference max (rescale O only when
+// the running max grows by more than 8, FA4-style); the entropy accumulator uses the
+// same reference, so  sum p ln p = ln2 * h / l - ln l  exactly as absorb_stats
+// (flash_entropy.hpp:25-51) but without per-tile rescaling.
+#include <cuda_bf16.h>
+
+#include "../internal.hpp"
+#include "sm100_ptx.cuh"
+
+namespace vmb {
+namespace {
+
+using namespace ptx;
+
+constexpr int kThreads = 256;
+constexpr int kTile = 128;                 // query rows per CTA, keys per KV tile
+constexpr uint32_t kPanelBytes = 128 * 128;  // 128 rows x 64 bf16
+constexpr uint32_t kTileBytes = 2 * kPanelBytes;  // 128 x 128 bf16
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kRescaleThreshold = 8.0f;
+constexpr float kMasked = -1.0e30f;
+
+template <int NB>
+struct Stages {
+    static constexpr int value = NB == 1 ? 4 : 3;
+};
+
+struct Params {
+    TcFaArgs a;
+    int32_t n_kv_tiles;
+};
+
+template <int NB, int NO>
+struct Smem {
+    static constexpr int S = Stages<NB>::value;
+    static constexpr uint32_t q_off = 0;
+    static constexpr uint32_t kv_off = kTileBytes;
+    static constexpr uint32_t bar_off = kv_off + S * NB * kTileBytes;
+    // barriers: q_full, kv_full[S], kv_empty[S], s_full[2], p_full[2], pv_done, o_full
+    static constexpr uint32_t n_bars = 1 + 2 * S + 2 + 2 + 2;
+    static constexpr uint32_t tmem_slot_off = bar_off + n_bars * 8;
+    static constexpr uint32_t bytes = tmem_slot_off + 16;
+    static constexpr uint32_t alloc = bytes + 1024;  // alignment slack
+};
+
+template <int NB, int NO>
+__global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constant__ Params p) {
+    using SM = Smem<NB, NO>;
+    constexpr int S = SM::S;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::bar_off);
+    uint64_t* q_full = bars;
+    uint64_t* kv_full = bars + 1;
+    uint64_t* kv_empty = bars + 1 + S;
+    uint64_t* s_full = bars + 1 + 2 * S;
+    uint64_t* p_full = bars + 3 + 2 * S;
+    uint64_t* pv_done = bars + 5 + 2 * S;
+    uint64_t* o_full = bars + 6 + 2 * S;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM::tmem_slot_off);
+
+    const TcFaArgs& a = p.a;
+    const int warp = warp_id();
+    const int qtile = blockIdx.x;
+    const int useg = blockIdx.y;           // u * nseg + s
+    const int u = useg / a.nseg, seg = useg % a.nseg;
+    const int n_kv = p.n_kv_tiles;
+
+    if (warp == 0 && elect_one()) {
+        tma_prefetch_desc(&a.tmQ);
+        tma_prefetch_desc(&a.tmK);
+        if (NB == 2) tma_prefetch_desc(&a.tmV);
+        mbar_init(q_full, 1);
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&kv_full[s], 1);
+            mbar_init(&kv_empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&s_full[s], 1);
+            mbar_init(&p_full[s], 128);
+        }
+        mbar_init(pv_done, 1);
+        mbar_init(o_full, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tS0 = tmem, tO = tmem + 256;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ TMA producer
+        if (elect_one()) {
+            const int qb = u / a.qH, qh = u % a.qH;
+            const int kb = u / a.kH, kh = u % a.kH;
+            const int kseg = seg;  // R-step: frame k of K; attention modes have nseg == 1
+            uint8_t* sq = smem + SM::q_off;
+            mbar_arrive_expect_tx(q_full, kTileBytes);
+            tma_load_5d(sq, &a.tmQ, q_full, 0, qtile * kTile, seg, qh, qb);
+            tma_load_5d(sq + kPanelBytes, &a.tmQ, q_full, 64, qtile * kTile, seg, qh, qb);
+            for (int j = 0; j < n_kv; ++j) {
+                const int st = j % S;
+                if (j >= S) mbar_wait(&kv_empty[st], ((j / S) + 1) & 1);
+                uint8_t* skv = smem + SM::kv_off + st * NB * kTileBytes;
+                mbar_arrive_expect_tx(&kv_full[st], NB * kTileBytes);
+                tma_load_5d(skv, &a.tmK, &kv_full[st], 0, j * kTile, kseg, kh, kb);
+                tma_load_5d(skv + kPanelBytes, &a.tmK, &kv_full[st], 64, j * kTile, kseg, kh, kb);
+                if (NB == 2) {
+                    tma_load_5d(skv + kTileBytes, &a.tmV, &kv_full[st], 0, j * kTile, kseg, kh, kb);
+                    tma_load_5d(skv + kTileBytes + kPanelBytes, &a.tmV, &kv_full[st], 64,
+                                j * kTile, kseg, kh, kb);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);   // S = Q K^T, both K-major
+        constexpr uint32_t idPV = idesc_bf16(128, 128, 0, 1);  // O += P V, V MN-major
+        const uint32_t q_addr = smem_u32(smem + SM::q_off);
+        const uint32_t kv_addr = smem_u32(smem + SM::kv_off);
+        if (elect_one()) {
+            mbar_wait(q_full, 0);
+            for (int j = 0; j <= n_kv; ++j) {
+                if (j < n_kv) {
+                    const int st = j % S;
+                    mbar_wait(&kv_full[st], (j / S) & 1);
+                    tc_fence_after();
+                    const uint32_t kaddr = kv_addr + st * NB * kTileBytes;
+                    const uint32_t tS = tS0 + (j & 1) * 128;
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const uint32_t off = (kk >> 2) * kPanelBytes + (kk & 3) * 32;
+                        umma_ss(tS, sdesc_sw128(q_addr + off, 16, 1024),
+                                sdesc_sw128(kaddr + off, 16, 1024), idS, kk > 0);
+                    }
+                    umma_commit(&s_full[j & 1]);
+                }
+                if (j >= 1) {
+                    const int jp = j - 1, st = jp % S;
+                    mbar_wait(&p_full[jp & 1], (jp >> 1) & 1);
+                    tc_fence_after();
+                    const uint32_t tP = tS0 + (jp & 1) * 128;
+                    const uint32_t kaddr = kv_addr + st * NB * kTileBytes;
+#pragma unroll
+                    for (int t = 0; t < NO; ++t) {
+                        // value operand: K tile (NB == 1, or t == 0 of [K|V]) else V tile
+                        const uint32_t vaddr = kaddr + ((NB == 2 && (NO == 1 || t == 1)) ? kTileBytes : 0);
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk) {
+                            umma_ts(tO + t * 128, tP + kk * 8,
+                                    sdesc_sw128(vaddr + kk * 2048, kPanelBytes, 1024), idPV,
+                                    (jp > 0 || kk > 0) ? 1u : 0u);
+                        }
+                    }
+                    umma_commit(&kv_empty[st]);
+                    umma_commit(pv_done);
+                }
+            }
+            umma_commit(o_full);
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------------------ softmax / epilogue
+        const int row = threadIdx.x - 128;            // TMEM lane == query row in tile
+        const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+        const int grow = qtile * kTile + row;         // row within the segment
+        const bool valid = grow < a.q_len;
+        float c = 1.f;
+        if (a.cR && valid) c = a.cR[((int64_t)u * a.nseg + seg) * a.q_len + grow];
+        if (a.clamp_enabled) {
+            c = (c < a.clamp_min) ? a.clamp_min : c;
+        } else if (!(c > 0.f)) {
+            if (valid) atomicExch(a.status, kStatusClampDomain);
+            c = 1.f;
+        }
+        const float scale2 = a.qscale * kLog2e / c;
+        const int last_valid = a.kv_len - (n_kv - 1) * kTile;  // valid keys in the last tile
+
+        if (a.check_finite) {
+            mbar_wait(q_full, 0);
+            const uint4* q0 = reinterpret_cast<const uint4*>(smem + SM::q_off + row * 128);
+            const uint4* q1 = reinterpret_cast<const uint4*>(smem + SM::q_off + kPanelBytes + row * 128);
+            bool bad = false;
+#pragma unroll
+            for (int x = 0; x < 8; ++x) {
+                const uint4 v0 = q0[x], v1 = q1[x];
+                const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    bad |= ((w[e] & 0x7F80u) == 0x7F80u) || ((w[e] & 0x7F800000u) == 0x7F800000u);
+            }
+            if (bad && valid) atomicExch(a.status, kStatusNonFiniteQ);
+        }
+
+        float m_run = -INFINITY, l_run = 0.f, h_run = 0.f;
+        for (int j = 0; j < n_kv; ++j) {
+            const uint32_t tS = tS0 + (j & 1) * 128 + lane_base;
+            mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+            tc_fence_after();
+            uint32_t sr[128];
+            VMB_TMEM_LD32(tS + 0, (sr + 0));
+            VMB_TMEM_LD32(tS + 32, (sr + 32));
+            VMB_TMEM_LD32(tS + 64, (sr + 64));
+            VMB_TMEM_LD32(tS + 96, (sr + 96));
+            tmem_ld_wait();
+            float* s = reinterpret_cast<float*>(sr);
+            if (j == n_kv - 1 && last_valid < kTile) {
+#pragma unroll
+                for (int x = 0; x < 128; ++x)
+                    if (x >= last_valid) s[x] = kMasked;
+            }
+            float tmax = s[0];
+#pragma unroll
+            for (int x = 1; x < 128; ++x) tmax = fmaxf(tmax, s[x]);
+            const float m_cand = tmax * scale2;
+            if (j == 0) {
+                m_run = m_cand;
+            } else {
+                const bool need = m_cand > m_run + kRescaleThreshold;
+                if (__any_sync(0xffffffffu, need)) {
+                    const float m_new = fmaxf(m_run, m_cand);
+                    const float alpha = ex2(m_run - m_new);
+                    h_run = alpha * (h_run + (m_run - m_new) * l_run);
+                    l_run *= alpha;
+                    m_run = m_new;
+                    // O must hold every earlier P V product before it is rescaled
+                    mbar_wait(pv_done, (j - 1) & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int t = 0; t < NO; ++t) {
+#pragma unroll
+                        for (int cc = 0; cc < 4; ++cc) {
+                            uint32_t orr[32];
+                            const uint32_t ta = tO + t * 128 + cc * 32 + lane_base;
+                            VMB_TMEM_LD32(ta, orr);
+                            tmem_ld_wait();
+#pragma unroll
+                            for (int x = 0; x < 32; ++x)
+                                orr[x] = __float_as_uint(__uint_as_float(orr[x]) * alpha);
+                            VMB_TMEM_ST32(ta, orr);
+                        }
+                    }
+                }
+            }
+            const float neg_m = -m_run;
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+                uint32_t pk[16];
+#pragma unroll
+                for (int x = 0; x < 16; ++x) {
+                    const float t0 = fmaf(s[cc * 32 + 2 * x], scale2, neg_m);
+                    const float t1 = fmaf(s[cc * 32 + 2 * x + 1], scale2, neg_m);
+                    const float p0 = ex2(t0), p1 = ex2(t1);
+                    l_run += p0 + p1;
+                    h_run = fmaf(p0, t0, fmaf(p1, t1, h_run));
+                    pk[x] = pack_bf16(p0, p1);
+                }
+                VMB_TMEM_ST16(tS + cc * 16, pk);
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&p_full[j & 1]);
+        }
+
+        // ------------------------------------------------------------ epilogue
+        mbar_wait(o_full, 0);
+        tc_fence_after();
+        const float inv_l = 1.f / l_run;
+        const int64_t ob = u / a.oHn, oh = u % a.oHn;
+#pragma unroll
+        for (int t = 0; t < NO; ++t) {
+            __nv_bfloat16* out = static_cast<__nv_bfloat16*>(t == 0 ? a.out0 : a.out1);
+            __nv_bfloat16* orow = out + ob * a.oB[t] + oh * a.oH[t] + (int64_t)seg * a.oS[t] +
+                                  (int64_t)grow * a.oR[t];
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+                uint32_t orr[32];
+                VMB_TMEM_LD32(tO + t * 128 + cc * 32 + lane_base, orr);
+                tmem_ld_wait();
+                if (valid) {
+                    uint4* dst = reinterpret_cast<uint4*>(orow + cc * 32);
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) {
+                        uint4 v;
+                        v.x = pack_bf16(__uint_as_float(orr[8 * x + 0]) * inv_l, __uint_as_float(orr[8 * x + 1]) * inv_l);
+                        v.y = pack_bf16(__uint_as_float(orr[8 * x + 2]) * inv_l, __uint_as_float(orr[8 * x + 3]) * inv_l);
+                        v.z = pack_bf16(__uint_as_float(orr[8 * x + 4]) * inv_l, __uint_as_float(orr[8 * x + 5]) * inv_l);
+                        v.w = pack_bf16(__uint_as_float(orr[8 * x + 6]) * inv_l, __uint_as_float(orr[8 * x + 7]) * inv_l);
+                        dst[x] = v;
+                    }
+                }
+            }
+        }
+        if (valid) {
+            const float ln_l = logf(l_run);
+            if (a.cl_out)
+                a.cl_out[((int64_t)u * a.q_len + grow) * a.nseg + seg] = kLn2 * h_run * inv_l - ln_l;
+            if (a.lse_out)
+                a.lse_out[((int64_t)u * a.nseg + seg) * a.q_len + grow] = kLn2 * (m_run + log2f(l_run));
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
+template <int NB, int NO>
+void launch(const Params& p, int64_t U, cudaStream_t s) {
+    using SM = Smem<NB, NO>;
+    auto kern = fa_tc_kernel<NB, NO>;
+    VMB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)SM::alloc));
+    dim3 grid((unsigned)((p.a.q_len + kTile - 1) / kTile), (unsigned)(U * p.a.nseg));
+    kern<<<grid, kThreads, SM::alloc, s>>>(p);
+    count_launch();
+    check_launch("fa_tc");
+}
+
+}  // namespace
+
+void tc_fa_launch(const TcFaArgs& a, int64_t U, cudaStream_t s) {
+    if (U == 0 || a.q_len == 0) return;
+    VMB_REQUIRE_DIM(a.kv_len >= 1, "attention over empty keys");
+    Params p;
+    p.a = a;
+    p.n_kv_tiles = (a.kv_len + kTile - 1) / kTile;
+    if (a.nv == 2) launch<2, 2>(p, U, s);
+    else if (a.v_is_k) launch<1, 1>(p, U, s);
+    else launch<2, 1>(p, U, s);
+}
+
+}  // namespace vmb

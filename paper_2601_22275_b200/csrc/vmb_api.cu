@@ -1,0 +1,748 @@
+// vmb_api.cu — the C ABI (include/vmb.h): validation, workspace, TMA maps and the
+// stream-ordered launch plan of the VMonarch forward.
+//
+// Launch plan of vmb_vmonarch_fwd (reference: video.hpp:84-150 + monarch.hpp:155-193),
+// all batch*head units batched into every launch:
+//   for t in [0, iters):
+//     R half-step      fa_tc <1,1>  (last iteration: <2,2>, y = R V fused)
+//     L half-step      lstep_tc ITER (last iteration: FINAL -> O, permutation folded)
+//   first-frame recompute  fa_tc <2,1> over Q[0:hw] x all keys -> O[0:hw)
+// Shapes outside the tcgen05 kernels' envelope (fp32 parity mode, d != 128, m > 128)
+// run the same plan on the CUDA-core kernels in kernels/simt.cu.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "internal.hpp"
+
+namespace vmb {
+
+std::atomic<uint64_t> g_launches{0};
+static thread_local std::string t_last_error;
+
+void set_error(const std::string& msg) { t_last_error = msg; }
+
+void check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        throw Error{VMB_ERR_CUDA, std::string("cuda error: launch of ") + what + ": " + cudaGetErrorString(e)};
+}
+
+// ---------------------------------------------------------------- TMA maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+bool tmap_supported() { return encode_fn() != nullptr; }
+
+CUtensorMap make_tmap_bf16_5d(const void* base, const uint64_t dims[5], const uint64_t strides_bytes[4],
+                              const uint32_t box[5]) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) throw Error{VMB_ERR_CUDA, "cuda error: cuTensorMapEncodeTiled unavailable"};
+    CUtensorMap map;
+    cuuint64_t gd[5], gs[4];
+    cuuint32_t bx[5], es[5] = {1, 1, 1, 1, 1};
+    for (int i = 0; i < 5; ++i) {
+        gd[i] = dims[i] > 0 ? dims[i] : 1;
+        bx[i] = box[i];
+    }
+    // strides of size-1 dims are irrelevant but must be valid (16-B multiple, < 2^40)
+    uint64_t prev = dims[0] * 2;
+    for (int i = 0; i < 4; ++i) {
+        uint64_t s = strides_bytes[i];
+        if (gd[i + 1] == 1 || s == 0) s = std::max<uint64_t>(prev, 16);
+        s = (s + 15) & ~uint64_t(15);
+        gs[i] = s;
+        prev = s * gd[i + 1];
+    }
+    CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), gd, gs, bx, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        char buf[256];
+        snprintf(buf, sizeof buf, "cuda error: cuTensorMapEncodeTiled failed (%d) dims %llu,%llu,%llu,%llu,%llu",
+                 (int)r, (unsigned long long)gd[0], (unsigned long long)gd[1], (unsigned long long)gd[2],
+                 (unsigned long long)gd[3], (unsigned long long)gd[4]);
+        throw Error{VMB_ERR_CUDA, buf};
+    }
+    return map;
+}
+
+namespace {
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
+
+struct Shape {
+    int64_t T, h, w, d, H, B, U, N, m, b, hw;
+};
+
+Shape make_shape(const vmb_grid* g, const vmb_config* c) {
+    VMB_REQUIRE_DIM(g && c, "null grid or config");
+    VMB_REQUIRE_DIM(g->t_frames >= 1 && g->h >= 1 && g->w >= 1, "grid dims must be positive");
+    VMB_REQUIRE_DIM(g->heads >= 0 && g->batch >= 0, "heads and batch must be non-negative");
+    VMB_REQUIRE_DIM(g->head_dim >= 1, "head dim must be >= 1");
+    VMB_REQUIRE_DIM(c->iters >= 1, "iteration count must be >= 1");
+    Shape s;
+    s.T = g->t_frames;
+    s.h = g->h;
+    s.w = g->w;
+    s.d = g->head_dim;
+    s.H = g->heads;
+    s.B = g->batch;
+    s.U = s.H * s.B;
+    s.N = s.T * s.h * s.w;
+    s.hw = s.h * s.w;
+    if (c->override_m != 0 || c->override_b != 0) {
+        VMB_REQUIRE_DIM(c->override_m >= 1 && c->override_b >= 1 && c->override_m * c->override_b == s.N,
+                        "override factor sizes must satisfy m*b = N");
+        s.m = c->override_m;
+        s.b = c->override_b;
+    } else {
+        s.m = s.T;
+        s.b = s.hw;
+    }
+    return s;
+}
+
+struct Workspace {
+    int32_t* status;
+    void* aR;
+    void* aL;
+    void* y;
+    float* cR;
+    float* cL;
+    size_t bytes;
+};
+
+Workspace carve(void* base, const Shape& s, vmb_dtype dt) {
+    const size_t es = dt == VMB_BF16 ? 2 : 4;
+    const size_t act = align_up((size_t)s.U * s.N * s.d * es);
+    const size_t st = align_up((size_t)s.U * s.N * sizeof(float));
+    uint8_t* p = static_cast<uint8_t*>(base);
+    Workspace w;
+    w.status = reinterpret_cast<int32_t*>(p);
+    size_t off = kAlign;
+    w.aR = p + off; off += act;
+    w.aL = p + off; off += act;
+    w.y = p + off; off += act;
+    w.cR = reinterpret_cast<float*>(p + off); off += st;
+    w.cL = reinterpret_cast<float*>(p + off); off += st;
+    w.bytes = off;
+    return w;
+}
+
+vmb_strides default_strides(const Shape& s) {
+    vmb_strides st;
+    st.token = s.d;
+    st.head = s.N * s.d;
+    st.batch = s.H * s.N * s.d;
+    return st;
+}
+
+// View of a user tensor with rows (u, frame, pos) -> token frame*b + pos.
+View user_view(const void* base, const vmb_strides& st, const Shape& s, int64_t a_stride_tokens,
+               int64_t c_stride_tokens) {
+    View v;
+    v.base = base;
+    v.sB = st.batch;
+    v.sH = st.head;
+    v.sa = a_stride_tokens * st.token;
+    v.sc = c_stride_tokens * st.token;
+    v.H = (int32_t)std::max<int64_t>(s.H, 1);
+    return v;
+}
+// Internal contiguous tensor: row (u, a, c) at u*unit + a*sa + c*sc.
+View internal_view(const void* base, int64_t unit, int64_t sa, int64_t sc) {
+    View v;
+    v.base = base;
+    v.sB = unit;
+    v.sH = 0;
+    v.sa = sa;
+    v.sc = sc;
+    v.H = 1;
+    return v;
+}
+// 5-D map over a user bf16 tensor: (d, pos, frame, head, batch) with token = frame*b + pos.
+CUtensorMap user_map(const void* base, const vmb_strides& st, const Shape& s, int64_t pos_len,
+                     int64_t pos_stride_tok, int64_t frames, int64_t frame_stride_tok, uint32_t box_pos,
+                     uint32_t box_frame) {
+    const uint64_t dims[5] = {(uint64_t)s.d, (uint64_t)pos_len, (uint64_t)frames,
+                              (uint64_t)std::max<int64_t>(s.H, 1), (uint64_t)std::max<int64_t>(s.B, 1)};
+    const uint64_t strides[4] = {(uint64_t)(pos_stride_tok * st.token * 2), (uint64_t)(frame_stride_tok * st.token * 2),
+                                 (uint64_t)(st.head * 2), (uint64_t)(st.batch * 2)};
+    const uint32_t box[5] = {64, box_pos, box_frame, 1, 1};
+    return make_tmap_bf16_5d(base, dims, strides, box);
+}
+// 5-D map over an internal contiguous (U, A, C, d) bf16 tensor; dim1 = c (or a), dim2 = a (or c).
+CUtensorMap internal_map(const void* base, int64_t U, int64_t A, int64_t C, int64_t d, bool dim1_is_c,
+                         uint32_t box1, uint32_t box2) {
+    uint64_t dims[5], strides[4];
+    dims[0] = (uint64_t)d;
+    if (dim1_is_c) {
+        dims[1] = (uint64_t)C; strides[0] = (uint64_t)(d * 2);
+        dims[2] = (uint64_t)A; strides[1] = (uint64_t)(C * d * 2);
+    } else {
+        dims[1] = (uint64_t)A; strides[0] = (uint64_t)(C * d * 2);
+        dims[2] = (uint64_t)C; strides[1] = (uint64_t)(d * 2);
+    }
+    dims[3] = 1; strides[2] = (uint64_t)(A * C * d * 2);
+    dims[4] = (uint64_t)U; strides[3] = (uint64_t)(A * C * d * 2);
+    const uint32_t box[5] = {64, box1, box2, 1, 1};
+    return make_tmap_bf16_5d(base, dims, strides, box);
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+bool tc_eligible(const Shape& s, vmb_dtype dt, const vmb_strides& in, const vmb_strides& out,
+                 const void* q, const void* k, const void* v, const void* o) {
+    if (dt != VMB_BF16 || s.d != 128 || s.m > 128 || !tmap_supported()) return false;
+    if (s.N > (int64_t)INT32_MAX || s.b > 65535 * 16) return false;
+    const int64_t strides[6] = {in.batch, in.head, in.token, out.batch, out.head, out.token};
+    for (int64_t x : strides)
+        if (x % 8 != 0) return false;
+    if (out.token % 8 != 0) return false;
+    return aligned16(q) && aligned16(k) && aligned16(v) && aligned16(o);
+}
+
+template <typename F>
+vmb_status guarded(F&& f) {
+    try {
+        f();
+        return VMB_OK;
+    } catch (const Error& e) {
+        set_error(e.msg);
+        return e.status;
+    } catch (const std::exception& e) {
+        set_error(std::string("error: ") + e.what());
+        return VMB_ERR_CUDA;
+    }
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// ---------------------------------------------------------------- the forward plan
+void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q, const void* k,
+             const void* v, void* o, const vmb_strides& in, const vmb_strides& out, const Workspace& ws,
+             cudaStream_t st) {
+    const bool bf16 = dt == VMB_BF16;
+    const float qscale = (float)(1.0 / std::sqrt((double)s.d));
+    const bool recompute = cfg.recompute_first_frame != 0;
+    const bool skip_j0 = recompute && s.b == s.hw;
+    const int64_t U = s.U, m = s.m, b = s.b, d = s.d;
+    VMB_CHECK_CUDA(cudaMemsetAsync(ws.status, 0, sizeof(int32_t), st));
+    if (U == 0) return;
+
+    if (tc_eligible(s, dt, in, out, q, k, v, o)) {
+        // ------------------------------------------------ tcgen05 path
+        const CUtensorMap mQrow = user_map(q, in, s, b, 1, m, b, 128, 1);    // (d, i, k): query tiles
+        const CUtensorMap mK = user_map(k, in, s, b, 1, m, b, 128, 1);
+        const CUtensorMap mV = user_map(v, in, s, b, 1, m, b, 128, 1);
+        const CUtensorMap mQcol = user_map(q, in, s, b, 1, m, b, 1, 128);    // (d, i, j): Qb[i] boxes
+        const CUtensorMap mAR = internal_map(ws.aR, U, m, b, d, true, 128, 1);  // aR (U,m,b,d)
+        const CUtensorMap mAL = internal_map(ws.aL, U, b, m, d, true, 128, 1);  // aL (U,b,m,d): (d,k,i)
+        const CUtensorMap mY = internal_map(ws.y, U, m, b, d, true, 1, 128);    // y (U,m,b,d): (d,i,k)
+        for (int64_t t = 0; t < cfg.iters; ++t) {
+            const bool last = t == cfg.iters - 1;
+            TcFaArgs fa{};
+            fa.tmQ = t == 0 ? mQrow : mAR;
+            fa.tmK = mK;
+            fa.tmV = mV;
+            fa.nseg = (int32_t)m;
+            fa.q_len = (int32_t)b;
+            fa.kv_len = (int32_t)b;
+            fa.qH = t == 0 ? (int32_t)std::max<int64_t>(s.H, 1) : 1;
+            fa.kH = (int32_t)std::max<int64_t>(s.H, 1);
+            fa.oHn = 1;
+            fa.cR = t == 0 ? nullptr : ws.cR;
+            fa.qscale = t == 0 ? qscale : 1.f;
+            fa.clamp_min = (float)cfg.clamp_min;
+            fa.clamp_enabled = cfg.clamp_enabled;
+            fa.nv = last ? 2 : 1;
+            fa.v_is_k = last ? 0 : 1;
+            fa.out0 = ws.aL;                       // aL (U, b, m, d): row (u, k, i)
+            fa.oB[0] = b * m * d; fa.oH[0] = 0; fa.oS[0] = d; fa.oR[0] = m * d;
+            fa.out1 = ws.y;                        // y (U, m, b, d): row (u, k, i)
+            fa.oB[1] = m * b * d; fa.oH[1] = 0; fa.oS[1] = b * d; fa.oR[1] = d;
+            fa.cl_out = ws.cL;
+            fa.lse_out = nullptr;
+            fa.status = ws.status;
+            fa.check_finite = t == 0;
+            tc_fa_launch(fa, U, st);
+
+            TcLstepArgs ls{};
+            ls.tmQ = mQcol;
+            ls.tmAL = mAL;
+            ls.tmY = mY;
+            ls.cL = ws.cL;
+            ls.qscale = qscale;
+            ls.m = (int32_t)m;
+            ls.b = (int32_t)b;
+            ls.H = (int32_t)std::max<int64_t>(s.H, 1);
+            ls.oHn = (int32_t)std::max<int64_t>(s.H, 1);
+            ls.final_mode = last;
+            ls.aR = static_cast<__nv_bfloat16*>(ws.aR);
+            ls.cR = ws.cR;
+            ls.ar_scale = qscale;
+            ls.O = static_cast<__nv_bfloat16*>(o);
+            ls.oB = out.batch; ls.oH = out.head; ls.oJ = b * out.token; ls.oI = out.token;
+            ls.skip_j0 = skip_j0;
+            tc_lstep_launch(ls, U, st);
+        }
+        if (recompute) {
+            TcFaArgs fa{};
+            fa.tmQ = user_map(q, in, s, s.hw, 1, 1, s.hw, 128, 1);
+            fa.tmK = user_map(k, in, s, s.N, 1, 1, s.N, 128, 1);
+            fa.tmV = user_map(v, in, s, s.N, 1, 1, s.N, 128, 1);
+            fa.nseg = 1;
+            fa.q_len = (int32_t)s.hw;
+            fa.kv_len = (int32_t)s.N;
+            fa.qH = fa.kH = fa.oHn = (int32_t)std::max<int64_t>(s.H, 1);
+            fa.cR = nullptr;
+            fa.qscale = qscale;
+            fa.clamp_enabled = 0;
+            fa.clamp_min = 0.f;
+            fa.nv = 1;
+            fa.v_is_k = 0;
+            fa.out0 = o;
+            fa.oB[0] = out.batch; fa.oH[0] = out.head; fa.oS[0] = 0; fa.oR[0] = out.token;
+            fa.status = ws.status;
+            tc_fa_launch(fa, U, st);
+        }
+        return;
+    }
+
+    // ---------------------------------------------------- CUDA-core path (any shape / fp32)
+    check_finite_rows(user_view(q, in, s, 0, 1), U, s.N, d, bf16, ws.status, st);
+    const View vQrow = user_view(q, in, s, b, 1);    // (u, k, i) -> token k*b+i
+    const View vK = user_view(k, in, s, b, 1);
+    const View vV = user_view(v, in, s, b, 1);
+    const View vQcol = user_view(q, in, s, 1, b);    // (u, i, j) -> token j*b+i
+    const int64_t ud = m * b * d;
+    const View vAR = internal_view(ws.aR, ud, b * d, d);      // (U,m,b,d) rows (u, k, i)
+    const View vAL_out = internal_view(ws.aL, ud, d, m * d);  // (U,b,m,d) rows (u, k, i)
+    const View vAL_in = internal_view(ws.aL, ud, m * d, d);   // (U,b,m,d) rows (u, i, k)
+    const View vY = internal_view(ws.y, ud, b * d, d);        // (U,m,b,d) rows (u, k, i)
+    for (int64_t t = 0; t < cfg.iters; ++t) {
+        const bool last = t == cfg.iters - 1;
+        SimtRstepArgs ra{};
+        ra.A = t == 0 ? vQrow : vAR;
+        ra.qscale = t == 0 ? qscale : 1.f;
+        ra.cR = t == 0 ? nullptr : ws.cR;
+        ra.clamp_min = (float)cfg.clamp_min;
+        ra.clamp_enabled = cfg.clamp_enabled;
+        ra.K = vK;
+        ra.V = vK;
+        ra.Out = vAL_out;
+        ra.cL = ws.cL;
+        ra.R = nullptr;
+        ra.U = U; ra.m = m; ra.b = b; ra.d = d;
+        ra.status = ws.status;
+        simt_rstep(ra, bf16, st);
+        if (last) {  // y = R V with the same R (monarch.hpp:182-185)
+            ra.V = vV;
+            ra.Out = vY;
+            ra.cL = nullptr;
+            simt_rstep(ra, bf16, st);
+        }
+        SimtLstepArgs la{};
+        la.Q = vQcol;
+        la.qscale = qscale;
+        la.aL = vAL_in;
+        la.cL = ws.cL;
+        la.aR = vAR;
+        la.cR = ws.cR;
+        la.Y = vY;
+        View vO = user_view(o, out, s, b, 1);  // (u, j, i) -> token j*b+i
+        la.O = vO;
+        la.skip_j0 = skip_j0;
+        la.L = nullptr;
+        la.final_mode = last;
+        la.U = U; la.m = m; la.b = b; la.d = d;
+        simt_lstep(la, bf16, st);
+    }
+    if (recompute) {
+        SimtFlashArgs fa{};
+        fa.Q = user_view(q, in, s, 0, 1);
+        fa.qscale = qscale;
+        fa.K = user_view(k, in, s, 0, 1);
+        fa.V = user_view(v, in, s, 0, 1);
+        fa.O = user_view(o, out, s, 0, 1);
+        fa.lse = nullptr;
+        fa.ent = nullptr;
+        fa.U = U; fa.nq = s.hw; fa.nk = s.N; fa.d = d;
+        simt_flash(fa, bf16, st);
+    }
+}
+
+}  // namespace
+}  // namespace vmb
+
+
+using namespace vmb;
+
+namespace {
+const vmb_strides* or_default(const vmb_strides* s, vmb_strides& tmp, const Shape& sh) {
+    if (s) return s;
+    tmp = default_strides(sh);
+    return &tmp;
+}
+int64_t ceil16(int64_t x) { return (x + 15) & ~int64_t(15); }
+}  // namespace
+
+extern "C" {
+
+const char* vmb_version(void) { return "vmonarch-b200 0.1 (sm_100a tcgen05)"; }
+const char* vmb_last_error(void) { return t_last_error.c_str(); }
+uint64_t vmb_kernel_launch_count(void) { return g_launches.load(); }
+
+void vmb_config_default(vmb_config* c) {
+    c->iters = 2;
+    c->clamp_min = 0.1;
+    c->clamp_enabled = 1;
+    c->recompute_first_frame = 1;
+    c->override_m = 0;
+    c->override_b = 0;
+    c->tile_br = 64;
+    c->tile_bc = 64;
+}
+
+vmb_status vmb_factorize(const vmb_grid* grid, const vmb_config* cfg, int64_t* m, int64_t* b) {
+    return guarded([&] {
+        VMB_REQUIRE_DIM(grid && cfg, "null grid or config");
+        VMB_REQUIRE_DIM(grid->t_frames >= 1 && grid->h >= 1 && grid->w >= 1, "grid dims must be positive");
+        const int64_t n = grid->t_frames * grid->h * grid->w;
+        if (cfg->override_m != 0 || cfg->override_b != 0) {
+            VMB_REQUIRE_DIM(cfg->override_m >= 1 && cfg->override_b >= 1 && cfg->override_m * cfg->override_b == n,
+                            "override factor sizes must satisfy m*b = N");
+            *m = cfg->override_m;
+            *b = cfg->override_b;
+        } else {
+            *m = grid->t_frames;
+            *b = grid->h * grid->w;
+        }
+    });
+}
+
+vmb_status vmb_make_perm(int64_t b, int64_t n, int64_t* fwd) {
+    return guarded([&] {
+        VMB_REQUIRE_DIM(b >= 1 && n >= 1, "permutation requires b >= 1 and n >= 1");
+        VMB_REQUIRE_DIM(n % b == 0, "permutation requires n divisible by b");
+        const int64_t m = n / b;
+        for (int64_t j = 0; j < b; ++j)
+            for (int64_t i = 0; i < m; ++i) fwd[j * m + i] = i * b + j;
+    });
+}
+
+vmb_status vmb_flops_estimate(const vmb_grid* grid, const vmb_config* cfg, int64_t d, double* sparsity,
+                              double* sparsity_approx, uint64_t* monarch, uint64_t* full, uint64_t* recomp,
+                              double* ratio) {
+    return guarded([&] {
+        int64_t m = 0, b = 0;
+        const vmb_status st = vmb_factorize(grid, cfg, &m, &b);
+        if (st != VMB_OK) throw Error{st, vmb_last_error()};
+        const uint64_t n = (uint64_t)m * (uint64_t)b, t = (uint64_t)cfg->iters, du = (uint64_t)d;
+        const uint64_t mb = (uint64_t)m + (uint64_t)b;
+        const double nn = (double)m * (double)b;
+        if (sparsity) *sparsity = 1.0 - (double)cfg->iters * ((double)m + (double)b) / nn;
+        if (sparsity_approx) *sparsity_approx = 1.0 - (double)cfg->iters / (double)m;
+        const uint64_t f = 4 * n * n * du;
+        const uint64_t mf = 2 * (2 * t * n * du * mb + n * du * mb);
+        const uint64_t rf = cfg->recompute_first_frame ? 4 * (uint64_t)(grid->h * grid->w) * n * du : 0;
+        if (full) *full = f;
+        if (monarch) *monarch = mf;
+        if (recomp) *recomp = rf;
+        if (ratio) *ratio = (double)f / (double)(mf + rf);
+    });
+}
+
+size_t vmb_workspace_size(const vmb_grid* grid, const vmb_config* cfg, vmb_dtype dtype) {
+    try {
+        const Shape s = make_shape(grid, cfg);
+        return carve(nullptr, s, dtype).bytes;
+    } catch (const Error& e) {
+        set_error(e.msg);
+        return 0;
+    }
+}
+
+vmb_status vmb_vmonarch_fwd(const vmb_grid* grid, const vmb_config* cfg, vmb_dtype dtype, const void* q,
+                            const void* k, const void* v, void* o, const vmb_strides* in_strides,
+                            const vmb_strides* out_strides, void* workspace, size_t ws_bytes, void* stream) {
+    return guarded([&] {
+        const Shape s = make_shape(grid, cfg);
+        VMB_REQUIRE_DIM(dtype == VMB_F32 || dtype == VMB_BF16, "unsupported dtype");
+        vmb_strides ti, to;
+        const vmb_strides* in = or_default(in_strides, ti, s);
+        const vmb_strides* out = or_default(out_strides, to, s);
+        VMB_REQUIRE_DIM(in->token >= s.d && out->token >= s.d, "token stride must be >= head dim");
+        const Workspace ws = carve(workspace, s, dtype);
+        VMB_REQUIRE_DIM(workspace != nullptr && ws_bytes >= ws.bytes, "workspace too small");
+        VMB_REQUIRE_DIM(s.U == 0 || (q && k && v && o), "null tensor pointer");
+        forward(s, *cfg, dtype, q, k, v, o, *in, *out, ws, as_stream(stream));
+    });
+}
+
+vmb_status vmb_workspace_status(void* workspace, void* stream) {
+    int32_t flag = 0;
+    vmb_status st = guarded([&] {
+        cudaStream_t s = as_stream(stream);
+        VMB_CHECK_CUDA(cudaMemcpyAsync(&flag, workspace, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        VMB_CHECK_CUDA(cudaStreamSynchronize(s));
+        VMB_CHECK_CUDA(cudaMemsetAsync(workspace, 0, sizeof(int32_t), s));
+    });
+    if (st != VMB_OK) return st;
+    if (flag == kStatusNonFiniteQ) {
+        set_error("domain error: Q contains non-finite values");
+        return VMB_ERR_DOMAIN;
+    }
+    if (flag == kStatusClampDomain) {
+        set_error("domain error: c_R <= 0 with clamping disabled");
+        return VMB_ERR_DOMAIN;
+    }
+    return VMB_OK;
+}
+
+vmb_status vmb_export_factors(const vmb_grid* grid, const vmb_config* cfg, vmb_dtype dtype, const void* q,
+                              const void* k, const vmb_strides* in_strides, void* workspace, float* L, float* R,
+                              void* stream) {
+    return guarded([&] {
+        const Shape s = make_shape(grid, cfg);
+        vmb_strides ti;
+        const vmb_strides* in = or_default(in_strides, ti, s);
+        const Workspace ws = carve(workspace, s, dtype);
+        const bool bf16 = dtype == VMB_BF16;
+        cudaStream_t st = as_stream(stream);
+        const int64_t m = s.m, b = s.b, d = s.d, ud = m * b * d;
+        const float qscale = (float)(1.0 / std::sqrt((double)d));
+        if (R) {
+            // R of the last R half-step, recomputed from that step's inputs, which the
+            // workspace still holds (aR/cR of iteration iters-2, or Q itself when iters == 1).
+            SimtRstepArgs ra{};
+            const bool first = cfg->iters == 1;
+            ra.A = first ? user_view(q, *in, s, b, 1) : internal_view(ws.aR, ud, b * d, d);
+            ra.qscale = first ? qscale : 1.f;
+            ra.cR = first ? nullptr : ws.cR;
+            ra.clamp_min = (float)cfg->clamp_min;
+            ra.clamp_enabled = cfg->clamp_enabled;
+            ra.K = user_view(k, *in, s, b, 1);
+            ra.V = ra.K;
+            ra.Out = internal_view(ws.y, ud, b * d, d);  // scratch: y is dead after the forward
+            ra.cL = nullptr;
+            ra.R = R;
+            ra.U = s.U; ra.m = m; ra.b = b; ra.d = d;
+            ra.status = ws.status;
+            simt_rstep(ra, bf16, st);
+        }
+        if (L) {
+            // L of the last L half-step from (Q, aL, cL); aR/cR are overwritten (scratch).
+            SimtLstepArgs la{};
+            la.Q = user_view(q, *in, s, 1, b);
+            la.qscale = qscale;
+            la.aL = internal_view(ws.aL, ud, m * d, d);
+            la.cL = ws.cL;
+            la.aR = internal_view(ws.aR, ud, b * d, d);
+            la.cR = ws.cR;
+            la.L = L;
+            la.final_mode = 0;
+            la.U = s.U; la.m = m; la.b = b; la.d = d;
+            simt_lstep(la, bf16, st);
+        }
+    });
+}
+
+vmb_status vmb_rstep(int64_t units, int64_t m, int64_t b, int64_t d, vmb_dtype dtype, const void* aR,
+                     const float* cR, const void* Kb, double clamp_min, int32_t clamp_enabled, void* aL, float* cL,
+                     float* R, void* stream) {
+    return guarded([&] {
+        VMB_REQUIRE_DIM(units >= 0 && m >= 1 && b >= 1 && d >= 1, "factor sizes must be >= 1");
+        cudaStream_t st = as_stream(stream);
+        const bool bf16 = dtype == VMB_BF16;
+        const int64_t ud = m * b * d;
+        if (!clamp_enabled) {
+            int32_t* flag = nullptr;
+            VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&flag), sizeof(int32_t), st));
+            VMB_CHECK_CUDA(cudaMemsetAsync(flag, 0, sizeof(int32_t), st));
+            check_clamp_domain(cR, units * m * b, flag, st);
+            int32_t h = 0;
+            VMB_CHECK_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+            VMB_CHECK_CUDA(cudaFreeAsync(flag, st));
+            VMB_CHECK_CUDA(cudaStreamSynchronize(st));
+            VMB_REQUIRE_DOMAIN(h == 0, "c_R <= 0 with clamping disabled");
+        }
+        const bool tc = bf16 && d == 128 && R == nullptr && tmap_supported() && aligned16(aR) && aligned16(Kb) &&
+                        aligned16(aL) && b <= INT32_MAX;
+        if (tc) {
+            TcFaArgs fa{};
+            fa.tmQ = internal_map(aR, units, m, b, d, true, 128, 1);
+            fa.tmK = internal_map(Kb, units, m, b, d, true, 128, 1);
+            fa.tmV = fa.tmK;
+            fa.nseg = (int32_t)m;
+            fa.q_len = fa.kv_len = (int32_t)b;
+            fa.qH = fa.kH = fa.oHn = 1;
+            fa.cR = cR;
+            fa.qscale = 1.f;
+            fa.clamp_min = (float)clamp_min;
+            fa.clamp_enabled = clamp_enabled;
+            fa.nv = 1;
+            fa.v_is_k = 1;
+            fa.out0 = aL;
+            fa.oB[0] = b * m * d; fa.oH[0] = 0; fa.oS[0] = d; fa.oR[0] = m * d;
+            fa.cl_out = cL;
+            fa.status = nullptr;
+            fa.check_finite = 0;
+            int32_t* dummy = nullptr;
+            VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dummy), sizeof(int32_t), st));
+            fa.status = dummy;
+            tc_fa_launch(fa, units, st);
+            VMB_CHECK_CUDA(cudaFreeAsync(dummy, st));
+            return;
+        }
+        int32_t* dummy = nullptr;
+        VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dummy), sizeof(int32_t), st));
+        SimtRstepArgs ra{};
+        ra.A = internal_view(aR, ud, b * d, d);
+        ra.qscale = 1.f;
+        ra.cR = cR;
+        ra.clamp_min = (float)clamp_min;
+        ra.clamp_enabled = clamp_enabled;
+        ra.K = internal_view(Kb, ud, b * d, d);
+        ra.V = ra.K;
+        ra.Out = internal_view(aL, ud, d, m * d);
+        ra.cL = cL;
+        ra.R = R;
+        ra.U = units; ra.m = m; ra.b = b; ra.d = d;
+        ra.status = dummy;
+        simt_rstep(ra, bf16, st);
+        VMB_CHECK_CUDA(cudaFreeAsync(dummy, st));
+    });
+}
+
+vmb_status vmb_lstep(int64_t units, int64_t m, int64_t b, int64_t d, vmb_dtype dtype, const void* Qb,
+                     const void* aL, const float* cL, void* aR, float* cR, float* L, void* stream) {
+    return guarded([&] {
+        VMB_REQUIRE_DIM(units >= 0 && m >= 1 && b >= 1 && d >= 1, "factor sizes must be >= 1");
+        cudaStream_t st = as_stream(stream);
+        const bool bf16 = dtype == VMB_BF16;
+        const int64_t ud = m * b * d;
+        const bool tc = bf16 && d == 128 && m <= 128 && L == nullptr && tmap_supported() && aligned16(Qb) &&
+                        aligned16(aL) && aligned16(aR);
+        (void)ceil16;
+        if (tc) {
+            TcLstepArgs ls{};
+            // Qb (U, b, m, d): rows (u, i, j); map dims (d, i, j, 1, U)
+            {
+                const uint64_t dims[5] = {(uint64_t)d, (uint64_t)b, (uint64_t)m, 1, (uint64_t)std::max<int64_t>(units, 1)};
+                const uint64_t strides[4] = {(uint64_t)(m * d * 2), (uint64_t)(d * 2), (uint64_t)(ud * 2), (uint64_t)(ud * 2)};
+                const uint32_t box[5] = {64, 1, 128, 1, 1};
+                ls.tmQ = make_tmap_bf16_5d(Qb, dims, strides, box);
+            }
+            ls.tmAL = internal_map(aL, units, b, m, d, true, 128, 1);
+            ls.tmY = ls.tmAL;
+            ls.cL = cL;
+            ls.qscale = 1.f;
+            ls.m = (int32_t)m;
+            ls.b = (int32_t)b;
+            ls.H = 1;
+            ls.oHn = 1;
+            ls.final_mode = 0;
+            ls.aR = static_cast<__nv_bfloat16*>(aR);
+            ls.cR = cR;
+            ls.ar_scale = 1.f;
+            tc_lstep_launch(ls, units, st);
+            return;
+        }
+        SimtLstepArgs la{};
+        la.Q = internal_view(Qb, ud, m * d, d);  // (U,b,m,d) rows (u, i, j)
+        la.qscale = 1.f;
+        la.aL = internal_view(aL, ud, m * d, d);
+        la.cL = cL;
+        la.aR = internal_view(aR, ud, b * d, d);
+        la.cR = cR;
+        la.L = L;
+        la.final_mode = 0;
+        la.U = units; la.m = m; la.b = b; la.d = d;
+        simt_lstep(la, bf16, st);
+    });
+}
+
+vmb_status vmb_flash_entropy_fwd(int64_t units, int64_t nq, int64_t nk, int64_t d, vmb_dtype dtype, const void* q,
+                                 const void* k, const void* v, float q_scale, void* o, float* lse, float* ent,
+                                 void* stream) {
+    return guarded([&] {
+        VMB_REQUIRE_DIM(units >= 0 && nq >= 0 && d >= 1, "bad attention shape");
+        VMB_REQUIRE_DOMAIN(nk >= 1, "attention over empty keys");
+        cudaStream_t st = as_stream(stream);
+        const bool bf16 = dtype == VMB_BF16;
+        const bool tc = bf16 && d == 128 && ent == nullptr && tmap_supported() && aligned16(q) && aligned16(k) &&
+                        aligned16(v) && aligned16(o) && nq <= INT32_MAX && nk <= INT32_MAX;
+        if (tc) {
+            TcFaArgs fa{};
+            const uint64_t sq = (uint64_t)(nq * d * 2), sk = (uint64_t)(nk * d * 2);
+            const uint64_t dq[5] = {(uint64_t)d, (uint64_t)nq, 1, 1, (uint64_t)std::max<int64_t>(units, 1)};
+            const uint64_t dk[5] = {(uint64_t)d, (uint64_t)nk, 1, 1, (uint64_t)std::max<int64_t>(units, 1)};
+            const uint64_t stq[4] = {(uint64_t)(d * 2), sq, sq, sq};
+            const uint64_t stk[4] = {(uint64_t)(d * 2), sk, sk, sk};
+            const uint32_t box[5] = {64, 128, 1, 1, 1};
+            fa.tmQ = make_tmap_bf16_5d(q, dq, stq, box);
+            fa.tmK = make_tmap_bf16_5d(k, dk, stk, box);
+            fa.tmV = make_tmap_bf16_5d(v, dk, stk, box);
+            fa.nseg = 1;
+            fa.q_len = (int32_t)nq;
+            fa.kv_len = (int32_t)nk;
+            fa.qH = fa.kH = fa.oHn = 1;
+            fa.qscale = q_scale;
+            fa.nv = 1;
+            fa.v_is_k = 0;
+            fa.out0 = o;
+            fa.oB[0] = nq * d; fa.oH[0] = 0; fa.oS[0] = 0; fa.oR[0] = d;
+            fa.lse_out = lse;
+            int32_t* dummy = nullptr;
+            VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dummy), sizeof(int32_t), st));
+            fa.status = dummy;
+            tc_fa_launch(fa, units, st);
+            VMB_CHECK_CUDA(cudaFreeAsync(dummy, st));
+            return;
+        }
+        SimtFlashArgs fa{};
+        fa.Q = internal_view(q, nq * d, 0, d);
+        fa.qscale = q_scale;
+        fa.K = internal_view(k, nk * d, 0, d);
+        fa.V = internal_view(v, nk * d, 0, d);
+        fa.O = internal_view(o, nq * d, 0, d);
+        fa.lse = lse;
+        fa.ent = ent;
+        fa.U = units; fa.nq = nq; fa.nk = nk; fa.d = d;
+        simt_flash(fa, bf16, st);
+    });
+}
+
+vmb_status vmb_dense_fwd(int64_t units, int64_t n, int64_t d, vmb_dtype dtype, const void* q, const void* k,
+                         const void* v, void* o, void* stream) {
+    return vmb_flash_entropy_fwd(units, n, n, d, dtype, q, k, v, (float)(1.0 / std::sqrt((double)d)), o, nullptr,
+                                 nullptr, stream);
+}
+
+vmb_status vmb_selftest_umma(int32_t mode, const void* A, const void* B, float* C, void* stream) {
+    return guarded([&] { selftest_umma(mode, A, B, C, as_stream(stream)); });
+}
+
+}  // extern "C"
