@@ -1,0 +1,381 @@
+"""bench.py — VMonarch attention forward on B200: ms/call at the 118K-token shape.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c4|c3|c2] [--no-cpu-baseline] [--no-e2e] [--no-dense]
+
+Workload (BASELINE.json metric, configs[3] = C4): 321-frame 448x832 video latent 81x28x52
+(N = 117,936 tokens), H = 40 heads, d = 128, bf16, t = 2, clamp 0.1, first-frame recompute
+on.  One "step" = one full vmonarch_attention call over all 40 heads.  With N GPUs the
+heads are sharded (40/N per GPU, no inter-GPU traffic) and the call time is the
+max over ranks (strong scaling: the 40-head call is fixed).
+
+Printed JSON line (rank 0): value = device-timed ms per call with inputs resident in HBM;
+e2e = the same call made with host (pinned) buffers, H2D/D2H copies inside the timed
+region; roofline = the dominant kernel's achieved TFLOP/s (algorithmic FLOPs per launch /
+CUDA-event launch time) against MEASURED_PEAKS.json; cpu_baseline = the reference CPU
+implementation (oracle/_ref, compiled from /root/reference) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+METRIC = "VMonarch attention ms/call at 118K tokens (H=40,d=128); TFLOPS vs tensor peak"
+CONFIGS = {
+    # name: (T, h, w, heads, d, description)
+    "c4": (81, 28, 52, 40, 128, "C4: 321-frame 448x832 latent 81x28x52 (N=117936), H=40, d=128, bf16, t=2"),
+    "c3": (21, 30, 52, 40, 128, "C3: Wan-2.1-14B 21x30x52 latent (N=32760), H=40, d=128, bf16, t=2"),
+    "c2": (21, 30, 52, 12, 128, "C2: Wan-2.1-1.3B 21x30x52 latent (N=32760), H=12, d=128, bf16, t=2"),
+}
+KERNEL_NAMES = ["rstep", "rstep_y", "attn_recompute", "lstep", "lstep_apply", "simt", "combine"]
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return {"hbm": p["hbm_gbs"], "bf16": p["bf16_tflops"], "bf16_sus": p.get("bf16_tflops_sustained"),
+                "src": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"hbm": 6650.0, "bf16": 1590.0, "bf16_sus": 1400.0, "src": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def flops_per_call(grid, vm):
+    cfg = vm.VMonarchConfig()
+    rep = vm.flops_estimate(grid, cfg, grid.head_dim)
+    return (rep.monarch_flops + rep.recompute_flops) * grid.units(), rep
+
+
+def kernel_algorithmic(grid, units):
+    """Algorithmic work per launch: FLOPs for tensor-bound, bytes for HBM-bound."""
+    N, d, m, b, hw = grid.tokens(), grid.head_dim, grid.t_frames, grid.h * grid.w, grid.h * grid.w
+    return {
+        "rstep": ("tensor", units * 4.0 * N * b * d),            # S = aR K^T, aL = P K
+        "rstep_y": ("tensor", units * 6.0 * N * b * d),          # + y = P V
+        "attn_recompute": ("tensor", units * 4.0 * hw * N * d),  # Q0 K^T, P V
+        "lstep": ("hbm", units * (3 * 2.0 * N * d + 2 * 4.0 * N)),        # Qb, aL in; aR out; cL in, cR out
+        "lstep_apply": ("hbm", units * (4 * 2.0 * N * d + 4.0 * N)),     # Qb, aL, y in; O out; cL in
+    }
+
+
+def cpu_reference_sample(cfgname: str, kind_pref: str = "reference", max_units: int | None = None):
+    """Time the reference CPU implementation on one wave of P units (P = host threads used)."""
+    import numpy as np
+    from oracle.oracle import Oracle, REF_SO, PORT_SO
+    T, h, w, heads, d, _ = CONFIGS[cfgname]
+    n = T * h * w
+    kind = "reference" if (kind_pref == "reference" and os.path.exists(REF_SO)) else "port"
+    orc = Oracle(kind)
+    cores = os.cpu_count() or 1
+    try:
+        import psutil
+        mem_units = int(psutil.virtual_memory().available / (2.5 * 2**30))
+    except Exception:
+        mem_units = 8
+    P = max(1, min(cores, heads, mem_units, max_units or heads))
+    rng = np.random.default_rng(0)
+    from oracle.oracle import bf16_round
+    q = bf16_round(rng.standard_normal((P, n, d), dtype=np.float32))
+    k = bf16_round(rng.standard_normal((P, n, d), dtype=np.float32))
+    v = bf16_round(rng.standard_normal((P, n, d), dtype=np.float32))
+    t0 = time.perf_counter()
+    orc.vmonarch_attention(q, k, v, (T, h, w), iters=2, threads=P)
+    wave = time.perf_counter() - t0
+    waves = math.ceil(heads / P)
+    ms = wave * waves * 1000.0
+    sample = (f"one wave of {P} of the {heads} head units of {cfgname.upper()} (vmonarch_attention<float>, "
+              f"{P} threads, bf16-rounded N(0,1) inputs), {wave:.1f} s; ms/call extrapolated x{waves} waves")
+    return {"value": round(ms, 1), "unit": "ms/call", "cores": P, "kind": kind, "sample": sample}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    T, h, w, heads, d, desc = CONFIGS[args.config]
+    steps = max(1, min(args.steps, 2))
+    vals = []
+    base = None
+    for _ in range(steps):
+        base = cpu_reference_sample(args.config)
+        vals.append(base["value"])
+    val = statistics.median(vals)
+    base["value"] = val
+    line = {
+        "metric": METRIC, "value": val, "unit": "ms/call", "n_gpus": args.gpus, "steps": steps, "warmup": 0,
+        "ms_per_step": val, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic N(0,1), bf16-rounded, f32 compute (reference CPU path)",
+        "config": {"workload": desc, "global_heads": heads, "seq_len": T * h * w,
+                   "parallelism": "CPU threads over head units"},
+        "impl": "reference", "cpu_baseline": base,
+        "e2e": {"value": val, "unit": "ms/call", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": f"{steps} step(s) of one CPU wave each (warm-up not meaningful for the CPU path); "
+                "bounded so the run ends within minutes",
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2601_22275_b200 as vm
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    T, h, w, heads, d, desc = CONFIGS[args.config]
+    # head sharding: contiguous blocks of heads per rank, no inter-GPU traffic
+    from paper_2601_22275_b200.dist import unit_shards
+    per = [b_ - a_ for a_, b_ in unit_shards(heads, world)]
+    my_heads = per[rank]
+    grid = vm.TokenGrid(T, h, w, d, my_heads, 1)
+    cfg = vm.VMonarchConfig()
+    n = grid.tokens()
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    q = torch.randn((my_heads, n, d), device=dev, dtype=torch.bfloat16, generator=gen)
+    k = torch.randn((my_heads, n, d), device=dev, dtype=torch.bfloat16, generator=gen)
+    v = torch.randn((my_heads, n, d), device=dev, dtype=torch.bfloat16, generator=gen)
+    o = torch.empty_like(q)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident timed region
+    vm.vmonarch_attention(q, k, v, grid, cfg, out=o, check=True)   # validates once (raises on error)
+    for _ in range(args.warmup):
+        vm.vmonarch_attention(q, k, v, grid, cfg, out=o, check=False)
+    torch.cuda.synchronize()
+    prof_enable = vm.lib.vmb_profile_enable
+    prof_enable.argtypes = [C.c_int32]
+    prof_read = vm.lib.vmb_profile_read
+    prof_read.argtypes = [C.c_void_p, C.c_void_p, C.c_int32]
+    ms_arr = (C.c_double * 7)()
+    cnt_arr = (C.c_uint64 * 7)()
+    prof_read(C.addressof(ms_arr), C.addressof(cnt_arr), 1)
+    sampler = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.15)
+    launches0 = vm.kernel_launch_count()
+    prof_enable(1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        vm.vmonarch_attention(q, k, v, grid, cfg, out=o, check=False)
+    e1.record()
+    torch.cuda.synchronize()
+    prof_enable(0)
+    launches = vm.kernel_launch_count() - launches0
+    clocks = sampler.stop()
+    barrier()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    ms = max_over_ranks(ms_local)
+    prof_read(C.addressof(ms_arr), C.addressof(cnt_arr), 1)
+    kern = {}
+    for i, nm in enumerate(KERNEL_NAMES):
+        if cnt_arr[i]:
+            kern[nm] = {"ms_per_launch": ms_arr[i] / cnt_arr[i], "launches": int(cnt_arr[i]),
+                        "share": ms_arr[i] / (ms_local * args.steps)}
+    finite = bool(torch.isfinite(o).all().item())
+
+    total_flops, rep = flops_per_call(vm.TokenGrid(T, h, w, d, heads, 1), vm)
+    tflops = total_flops / (ms * 1e-3) / 1e12
+    peaks = load_peaks()
+    # dominant kernel roofline
+    alg = kernel_algorithmic(grid, my_heads)
+    dom = max((k_ for k_ in kern if k_ in alg), key=lambda k_: kern[k_]["share"], default=None)
+    roof = None
+    if dom:
+        bound, work = alg[dom]
+        t = kern[dom]["ms_per_launch"] * 1e-3
+        if bound == "tensor":
+            ach, peak, unit = work / t / 1e12, peaks["bf16"], "TFLOP/s"
+        else:
+            ach, peak, unit = work / t / 1e9, peaks["hbm"], "GB/s"
+        traffic = None
+        try:
+            with open(os.path.join(HERE, "profiles", "ncu_traffic.json")) as f:
+                traffic = json.load(f).get(dom)
+        except Exception:
+            pass
+        roof = {"kernel": dom, "bound": bound, "achieved": round(ach, 1), "peak": peak, "unit": unit,
+                "frac": round(ach / peak, 4), "traffic": traffic, "peak_src": peaks["src"],
+                "algorithmic_per_launch": work}
+    for k_, (bound, work) in alg.items():
+        if k_ in kern:
+            t = kern[k_]["ms_per_launch"] * 1e-3
+            kern[k_]["achieved"] = round(work / t / (1e12 if bound == "tensor" else 1e9), 1)
+            kern[k_]["unit"] = "TFLOP/s" if bound == "tensor" else "GB/s"
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        hq = torch.empty(q.shape, dtype=q.dtype, pin_memory=True)
+        hk = torch.empty(k.shape, dtype=k.dtype, pin_memory=True)
+        hv = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
+        ho = torch.empty(o.shape, dtype=o.dtype, pin_memory=True)
+        hq.copy_(q); hk.copy_(k); hv.copy_(v)
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+
+        def e2e_step():
+            dq.copy_(hq, non_blocking=True)
+            dk.copy_(hk, non_blocking=True)
+            dv.copy_(hv, non_blocking=True)
+            vm.vmonarch_attention(dq, dk, dv, grid, cfg, out=o, check=False)
+            ho.copy_(o, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        e0.record()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.e2e_steps)
+        e2e = {"value": round(e2e_ms, 3), "unit": "ms/call",
+               "h2d_bytes_per_step": 3 * q.numel() * q.element_size(),
+               "d2h_bytes_per_step": o.numel() * o.element_size(),
+               "path": "pinned host Q/K/V -> HBM, vmonarch_attention (libvmb C ABI), O -> pinned host"}
+
+    # ---- dense FlashAttention-style bf16 baseline on the same GPU (same heads)
+    dense = None
+    if not args.no_dense:
+        od = torch.empty_like(q)
+        vm.dense_forward(q[:1], k[:1], v[:1])
+        torch.cuda.synchronize()
+        e0.record()
+        vm.lib.vmb_dense_fwd  # noqa
+        od = vm.dense_forward(q, k, v)
+        e1.record()
+        torch.cuda.synchronize()
+        dms = max_over_ranks(e0.elapsed_time(e1))
+        dflops = 4.0 * n * n * d * heads
+        dense = {"ms_per_call": round(dms, 2), "tflops": round(dflops / (dms * 1e-3) / 1e12, 1),
+                 "speedup_vmonarch_vs_dense": round(dms / ms, 2),
+                 "kernel": "libvmb fa_tc attention mode (tcgen05, same kernel family), 1 timed call"}
+        del od
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_sample(args.config)
+        except Exception as ex:  # noqa
+            cpu = {"value": None, "unit": "ms/call", "cores": 0, "kind": "unavailable", "sample": repr(ex)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(ms, 3), "unit": "ms/call", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic N(0,1) bf16 Q/K/V (torch.Generator seed 1234+rank), resident in HBM",
+            "config": {"workload": desc, "global_heads": heads, "heads_per_gpu": per, "seq_len": n,
+                       "parallelism": f"heads/{world}" if world > 1 else "single GPU",
+                       "l2": "inputs 1.2 GB per tensor (>126 MB L2); no flush needed"},
+            "tflops": round(tflops, 1), "tflops_frac_of_peak": round(tflops / peaks["bf16"], 4),
+            "algorithmic_flops_per_call": total_flops,
+            "roofline": roof, "kernels": kern, "e2e": e2e, "dense_baseline": dense, "cpu_baseline": cpu,
+            "clocks": clocks, "gpu_launches": launches, "output_finite": finite,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -136,6 +136,12 @@ vmb_status vmb_dense_fwd(int64_t units, int64_t n, int64_t d, vmb_dtype dtype, c
 /* ---- diagnostics ---- */
 /* Number of kernels the library launched since load (all entry points). */
 uint64_t vmb_kernel_launch_count(void);
+/* Per-kernel CUDA-event timing (off by default).  Kernel ids: 0 R half-step, 1 last R
+ * half-step (+ y), 2 attention (recompute / dense), 3 L half-step, 4 L half-step + apply,
+ * 5 CUDA-core kernels, 6 split-KV combine.  vmb_profile_read fills up to 7 entries and
+ * returns the count. */
+void vmb_profile_enable(int32_t on);
+int32_t vmb_profile_read(double* ms, uint64_t* counts, int32_t reset);
 /* Self-test of the tcgen05/TMA building blocks: mode 0 C = A B^T, 1 C = A B,
  * 2 C = A B with A staged in TMEM.  A, B (128x128 bf16 row-major), C (128x128 f32). */
 vmb_status vmb_selftest_umma(int32_t mode, const void* A, const void* B, float* C, void* stream);

@@ -37,6 +37,26 @@ struct Error {
 
 extern std::atomic<uint64_t> g_launches;
 inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// Optional per-kernel CUDA-event timing (vmb_profile_enable): a scope records an event
+// pair on the launching stream around one kernel launch; vmb_profile_read sums them.
+enum KernelId : int {
+    kKRstep = 0,      // fa_tc R half-step (NB=1, NO=1)
+    kKRstepY = 1,     // fa_tc last R half-step with y = R V fused (NB=2, NO=2)
+    kKAttn = 2,       // fa_tc recompute / dense attention (NB=2, NO=1)
+    kKLstep = 3,      // lstep_tc ITER
+    kKLfinal = 4,     // lstep_tc FINAL (apply)
+    kKSimt = 5,       // CUDA-core kernels
+    kKCombine = 6,    // split-KV combine
+    kKNum = 7
+};
+struct ProfScope {
+    ProfScope(int id, cudaStream_t s);
+    ~ProfScope();
+    int id;
+    cudaStream_t s;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+};
 // Throws on a launch error of the kernel just enqueued.
 void check_launch(const char* what);
 

@@ -337,6 +337,7 @@ void launch(const Params& p, int64_t U, cudaStream_t s) {
     VMB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)SM::alloc));
     dim3 grid((unsigned)((p.a.q_len + kTile - 1) / kTile), (unsigned)(U * p.a.nseg));
+    ProfScope ps(NO == 2 ? kKRstepY : (NB == 1 ? kKRstep : kKAttn), s);
     kern<<<grid, kThreads, SM::alloc, s>>>(p);
     count_launch();
     check_launch("fa_tc");

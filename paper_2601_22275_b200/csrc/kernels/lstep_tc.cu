@@ -228,6 +228,7 @@ void launch(const Params& p, int64_t U, cudaStream_t s) {
     auto kern = lstep_tc_kernel<FINAL>;
     VMB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM::alloc));
     dim3 grid((unsigned)p.a.b, (unsigned)U);
+    ProfScope ps(FINAL ? kKLfinal : kKLstep, s);
     kern<<<grid, kThreads, SM::alloc, s>>>(p);
     count_launch();
     check_launch("lstep_tc");

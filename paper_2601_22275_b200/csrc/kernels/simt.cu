@@ -403,6 +403,7 @@ void rstep_launch(const SimtRstepArgs& a, cudaStream_t s) {
     dim3 grid((unsigned)((a.b + RPB - 1) / RPB), (unsigned)a.m, (unsigned)a.U);
     const size_t smem = 2 * KTILE * a.d * sizeof(float);
     set_smem(simt_rstep_kernel<T, G>, smem);
+    ProfScope ps(kKSimt, s);
     simt_rstep_kernel<T, G><<<grid, BLOCK, smem, s>>>(a);
     count_launch();
     check_launch("simt_rstep");
@@ -412,6 +413,7 @@ void lstep_launch(const SimtLstepArgs& a, cudaStream_t s) {
     dim3 grid((unsigned)a.b, (unsigned)a.U);
     const size_t smem = 2 * a.m * sizeof(float);
     set_smem(simt_lstep_kernel<T, G>, smem);
+    ProfScope ps(kKSimt, s);
     simt_lstep_kernel<T, G><<<grid, BLOCK, smem, s>>>(a);
     count_launch();
     check_launch("simt_lstep");
@@ -422,6 +424,7 @@ void flash_launch(const SimtFlashArgs& a, cudaStream_t s) {
     dim3 grid((unsigned)((a.nq + RPB - 1) / RPB), (unsigned)a.U);
     const size_t smem = 2 * KTILE * a.d * sizeof(float);
     set_smem(simt_flash_kernel<T, G>, smem);
+    ProfScope ps(kKSimt, s);
     simt_flash_kernel<T, G><<<grid, BLOCK, smem, s>>>(a);
     count_launch();
     check_launch("simt_flash");

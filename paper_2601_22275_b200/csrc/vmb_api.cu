@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "internal.hpp"
 
@@ -25,6 +26,36 @@ std::atomic<uint64_t> g_launches{0};
 static thread_local std::string t_last_error;
 
 void set_error(const std::string& msg) { t_last_error = msg; }
+
+// ---------------------------------------------------------------- optional kernel timing
+namespace {
+struct ProfState {
+    std::mutex mu;
+    bool enabled = false;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+    double ms[kKNum] = {};
+    uint64_t count[kKNum] = {};
+};
+ProfState& prof() {
+    static ProfState p;
+    return p;
+}
+}  // namespace
+
+ProfScope::ProfScope(int id_, cudaStream_t s_) : id(id_), s(s_) {
+    ProfState& p = prof();
+    if (!p.enabled) return;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, s);
+}
+ProfScope::~ProfScope() {
+    if (!e0) return;
+    cudaEventRecord(e1, s);
+    ProfState& p = prof();
+    std::lock_guard<std::mutex> lk(p.mu);
+    p.pending.push_back({id, {e0, e1}});
+}
 
 void check_launch(const char* what) {
     cudaError_t e = cudaGetLastError();
@@ -739,6 +770,38 @@ vmb_status vmb_dense_fwd(int64_t units, int64_t n, int64_t d, vmb_dtype dtype, c
                          const void* v, void* o, void* stream) {
     return vmb_flash_entropy_fwd(units, n, n, d, dtype, q, k, v, (float)(1.0 / std::sqrt((double)d)), o, nullptr,
                                  nullptr, stream);
+}
+
+void vmb_profile_enable(int32_t on) {
+    ProfState& p = prof();
+    std::lock_guard<std::mutex> lk(p.mu);
+    p.enabled = on != 0;
+}
+
+// Resolves pending event pairs (synchronising on them), adds to the totals, and copies
+// per-kernel milliseconds / launch counts (kKNum entries each); reset != 0 clears.
+int32_t vmb_profile_read(double* ms, uint64_t* counts, int32_t reset) {
+    ProfState& p = prof();
+    std::lock_guard<std::mutex> lk(p.mu);
+    for (auto& e : p.pending) {
+        float t = 0.f;
+        cudaEventSynchronize(e.second.second);
+        cudaEventElapsedTime(&t, e.second.first, e.second.second);
+        p.ms[e.first] += t;
+        p.count[e.first] += 1;
+        cudaEventDestroy(e.second.first);
+        cudaEventDestroy(e.second.second);
+    }
+    p.pending.clear();
+    for (int i = 0; i < kKNum; ++i) {
+        if (ms) ms[i] = p.ms[i];
+        if (counts) counts[i] = p.count[i];
+        if (reset) {
+            p.ms[i] = 0;
+            p.count[i] = 0;
+        }
+    }
+    return kKNum;
 }
 
 vmb_status vmb_selftest_umma(int32_t mode, const void* A, const void* B, float* C, void* stream) {

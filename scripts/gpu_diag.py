@@ -1,6 +1,6 @@
 """Staged GPU diagnostics (run one stage per process under `timeout`).
 
-    python tests/gpu_diag.py <stage>
+    python scripts/gpu_diag.py <stage>
 
 Stages: selftest, rstep, lstep, flash, fwd_f32, fwd_bf16, fwd_big.  Prints max / rel-Fro errors
 against torch or the CPU oracle.  Used while bringing up kernels; the pytest suite holds the
