@@ -149,24 +149,22 @@ struct TcFaArgs {
 };
 void tc_fa_launch(const TcFaArgs& a, int64_t U, cudaStream_t s);
 
+// All L-step tiles are boxes of `rows = lstep_rows(m)` rows (m rounded up to 16); rows
+// >= m are OOB (zero-filled on load, clipped on store).
+inline int32_t lstep_rows(int64_t m) { return (int32_t)((m + 15) & ~int64_t(15)); }
 struct TcLstepArgs {
-    CUtensorMap tmQ;    // Q rows, 5-D (d, i, j, head, batch): Qb[i][j]
-    CUtensorMap tmAL;   // aL rows, 5-D (d, k, i, unit, 1)
-    CUtensorMap tmY;    // y rows, 5-D (d, i, k, unit, 1) (final mode)
+    CUtensorMap tmQ;    // Q rows, 5-D (d, i, j, head, batch): Qb[i][j], box (64, 1, rows)
+    CUtensorMap tmAL;   // aL rows, 5-D (d, k, i, 1, unit), box (64, rows, 1)
+    CUtensorMap tmY;    // FINAL: y rows, 5-D (d, i, k, 1, unit), box (64, 1, rows)
+    CUtensorMap tmOut;  // ITER: aR rows (d, i, k, 1, unit); FINAL: O rows (d, i, j, head, batch); box (64, 1, rows)
     const float* cL;    // (U, b, m)
     float qscale;
     int32_t m, b;
     int32_t H;          // heads per batch of the Q map
-    int32_t oHn;        // heads per batch of O
+    int32_t oHn;        // heads per batch of the output map (FINAL)
     int32_t final_mode;
-    // ITER outputs
-    __nv_bfloat16* aR;  // (U, m, b, d) contiguous
-    float* cR;          // (U, m, b)
-    float ar_scale;     // multiplies the aR epilogue
-    // FINAL outputs: O row (u, j, i) at O + (u/H)*oB + (u%H)*oH + j*oJ + i*oI
-    __nv_bfloat16* O;
-    int64_t oB, oH, oJ, oI;
-    int32_t skip_j0;
+    float* cR;          // ITER: (U, m, b)
+    float out_scale;    // multiplies the epilogue (ITER: aR scale)
 };
 void tc_lstep_launch(const TcLstepArgs& a, int64_t U, cudaStream_t s);
 

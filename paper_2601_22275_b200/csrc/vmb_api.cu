@@ -287,10 +287,13 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
         const CUtensorMap mQrow = user_map(q, in, s, b, 1, m, b, 128, 1);    // (d, i, k): query tiles
         const CUtensorMap mK = user_map(k, in, s, b, 1, m, b, 128, 1);
         const CUtensorMap mV = user_map(v, in, s, b, 1, m, b, 128, 1);
-        const CUtensorMap mQcol = user_map(q, in, s, b, 1, m, b, 1, 128);    // (d, i, j): Qb[i] boxes
-        const CUtensorMap mAR = internal_map(ws.aR, U, m, b, d, true, 128, 1);  // aR (U,m,b,d)
-        const CUtensorMap mAL = internal_map(ws.aL, U, b, m, d, true, 128, 1);  // aL (U,b,m,d): (d,k,i)
-        const CUtensorMap mY = internal_map(ws.y, U, m, b, d, true, 1, 128);    // y (U,m,b,d): (d,i,k)
+        const uint32_t lrows = (uint32_t)lstep_rows(m);
+        const CUtensorMap mQcol = user_map(q, in, s, b, 1, m, b, 1, lrows);   // (d, i, j): Qb[i] boxes
+        const CUtensorMap mAR = internal_map(ws.aR, U, m, b, d, true, 128, 1);  // aR (U,m,b,d): (d,i,k) query tiles
+        const CUtensorMap mARst = internal_map(ws.aR, U, m, b, d, true, 1, lrows);  // aR columns (d,i,k) for the L-step store
+        const CUtensorMap mAL = internal_map(ws.aL, U, b, m, d, true, lrows, 1);  // aL (U,b,m,d): (d,k,i)
+        const CUtensorMap mY = internal_map(ws.y, U, m, b, d, true, 1, lrows);    // y (U,m,b,d): (d,i,k)
+        const CUtensorMap mOcol = user_map(o, out, s, b, 1, m, b, 1, lrows);  // O rows j*b+i: (d, i, j)
         for (int64_t t = 0; t < cfg.iters; ++t) {
             const bool last = t == cfg.iters - 1;
             TcFaArgs fa{};
@@ -323,6 +326,7 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
             ls.tmQ = mQcol;
             ls.tmAL = mAL;
             ls.tmY = mY;
+            ls.tmOut = last ? mOcol : mARst;
             ls.cL = ws.cL;
             ls.qscale = qscale;
             ls.m = (int32_t)m;
@@ -330,12 +334,8 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
             ls.H = (int32_t)std::max<int64_t>(s.H, 1);
             ls.oHn = (int32_t)std::max<int64_t>(s.H, 1);
             ls.final_mode = last;
-            ls.aR = static_cast<__nv_bfloat16*>(ws.aR);
             ls.cR = ws.cR;
-            ls.ar_scale = qscale;
-            ls.O = static_cast<__nv_bfloat16*>(o);
-            ls.oB = out.batch; ls.oH = out.head; ls.oJ = b * out.token; ls.oI = out.token;
-            ls.skip_j0 = skip_j0;
+            ls.out_scale = last ? 1.f : qscale;
             tc_lstep_launch(ls, U, st);
         }
         if (recompute) {
@@ -679,15 +679,17 @@ vmb_status vmb_lstep(int64_t units, int64_t m, int64_t b, int64_t d, vmb_dtype d
         (void)ceil16;
         if (tc) {
             TcLstepArgs ls{};
+            const uint32_t lrows = (uint32_t)lstep_rows(m);
             // Qb (U, b, m, d): rows (u, i, j); map dims (d, i, j, 1, U)
             {
                 const uint64_t dims[5] = {(uint64_t)d, (uint64_t)b, (uint64_t)m, 1, (uint64_t)std::max<int64_t>(units, 1)};
                 const uint64_t strides[4] = {(uint64_t)(m * d * 2), (uint64_t)(d * 2), (uint64_t)(ud * 2), (uint64_t)(ud * 2)};
-                const uint32_t box[5] = {64, 1, 128, 1, 1};
+                const uint32_t box[5] = {64, 1, lrows, 1, 1};
                 ls.tmQ = make_tmap_bf16_5d(Qb, dims, strides, box);
             }
-            ls.tmAL = internal_map(aL, units, b, m, d, true, 128, 1);
+            ls.tmAL = internal_map(aL, units, b, m, d, true, lrows, 1);
             ls.tmY = ls.tmAL;
+            ls.tmOut = internal_map(aR, units, m, b, d, true, 1, lrows);
             ls.cL = cL;
             ls.qscale = 1.f;
             ls.m = (int32_t)m;
@@ -695,9 +697,8 @@ vmb_status vmb_lstep(int64_t units, int64_t m, int64_t b, int64_t d, vmb_dtype d
             ls.H = 1;
             ls.oHn = 1;
             ls.final_mode = 0;
-            ls.aR = static_cast<__nv_bfloat16*>(aR);
             ls.cR = cR;
-            ls.ar_scale = 1.f;
+            ls.out_scale = 1.f;
             tc_lstep_launch(ls, units, st);
             return;
         }
