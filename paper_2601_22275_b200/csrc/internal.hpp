@@ -149,6 +149,38 @@ struct TcFaArgs {
 };
 void tc_fa_launch(const TcFaArgs& a, int64_t U, cudaStream_t s);
 
+// fa2_tc.cu: 2 CTAs/SM flash attention with one value operand (R half-step: value = key,
+// BN = 128; attention: separate V, BN = 64, optional split-KV + combine).
+struct Tc2Args {
+    CUtensorMap tmQ, tmK, tmV;   // 5-D maps (d, row, seg, head, batch); Q box rows 128, K/V box rows tc2_kv_tile(nv)
+    int32_t nseg;                // segments per unit
+    int32_t q_len, kv_len;       // rows per segment
+    int32_t qH, kH, oHn;         // heads per batch of the q map, the k/v maps, the output
+    const float* cR;             // per-row temperature source (U, nseg, q_len) or nullptr
+    float qscale;                // logits multiplier (log2e applied inside)
+    float clamp_min;
+    int32_t clamp_enabled;
+    int32_t nv;                  // 1: value = key tile (R-step); 2: separate V
+    // output row (u, s, r) at out + (u/oHn)*oB + (u%oHn)*oH + s*oS + r*oR (bf16)
+    void* out;
+    int64_t oB, oH, oS, oR;
+    float* cl_out;               // sum p ln p per row: (u, r, s) at (u*q_len + r)*nseg + s   (nv == 1 only)
+    float* lse_out;              // natural-log lse: (u, s, r) at (u*nseg + s)*q_len + r
+    int32_t* status;
+    int32_t check_finite;
+    // split-KV (attention): fp32 partials (n_useg, nsplit, q_len, 128) + lse (n_useg, nsplit, q_len)
+    float* part_o;
+    float* part_lse;
+    int32_t max_split;           // 1 disables split-KV
+    int32_t nsplit;              // set by the launcher
+    int64_t n_useg;              // set by the launcher
+};
+int tc2_kv_tile(int nv);
+int tc2_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg, int nv, int max_split);
+// Largest split count tc2_fa_launch may pick (sizes the partial buffers).
+constexpr int kTc2MaxSplit = 16;
+void tc2_fa_launch(Tc2Args a, int64_t U, cudaStream_t s);
+
 // All L-step tiles are boxes of `rows = lstep_rows(m)` rows (m rounded up to 16); rows
 // >= m are OOB (zero-filled on load, clipped on store).
 inline int32_t lstep_rows(int64_t m) { return (int32_t)((m + 15) & ~int64_t(15)); }

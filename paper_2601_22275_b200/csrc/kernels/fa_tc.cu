@@ -41,6 +41,24 @@ constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescaleThreshold = 8.0f;
 constexpr float kMasked = -1.0e30f;
 
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+// 2^x on the FMA/ALU pipes: n = rint(x) via the 1.5*2^23 magic, 2^(x-n) by a degree-3
+// minimax polynomial on [-0.5, 0.5] (rel. err 1.1e-4, far below bf16 P rounding), then n is
+// added to the exponent field.  x is clamped at -126 (2^-126 is 0 for every purpose here).
+__device__ __forceinline__ float ex2_emu(float x) {
+    x = fmaxf(x, -126.f);
+    const float kMagic = 12582912.f;
+    const float t = x + kMagic;
+    const float f = x - (t - kMagic);
+    const float p = fmaf(fmaf(fmaf(0.05592203512787819f, f, 0.24264007806777954f), f, 0.6931210160255432f), f,
+                         0.9999244809150696f);
+    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 template <int NB>
 struct Stages {
     static constexpr int value = NB == 1 ? 4 : 3;
@@ -205,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
             bool bad = false;
 #pragma unroll
             for (int x = 0; x < 8; ++x) {
-                const uint4 v0 = q0[x], v1 = q1[x];
+                const uint4 v0 = q0[x ^ (row & 7)], v1 = q1[x ^ (row & 7)];
                 const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
                 for (int e = 0; e < 8; ++e)
@@ -214,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
             if (bad && valid) atomicExch(a.status, kStatusNonFiniteQ);
         }
 
-        float m_run = -INFINITY, l_run = 0.f, h_run = 0.f;
+        float m_run = -INFINITY, l_run = 0.f;
         for (int j = 0; j < n_kv; ++j) {
             const uint32_t tS = tS0 + (j & 1) * 128 + lane_base;
             mbar_wait(&s_full[j & 1], (j >> 1) & 1);
@@ -231,10 +249,18 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
                 for (int x = 0; x < 128; ++x)
                     if (x >= last_valid) s[x] = kMasked;
             }
-            float tmax = s[0];
+            // row max: 4 independent FMNMX3 chains (depth 16) instead of one of depth 127
+            float a0 = s[0], a1 = s[1], a2 = s[2], a3 = s[3];
 #pragma unroll
-            for (int x = 1; x < 128; ++x) tmax = fmaxf(tmax, s[x]);
-            const float m_cand = tmax * scale2;
+            for (int x = 4; x < 124; x += 8) {
+                a0 = fmax3(a0, s[x + 0], s[x + 1]);
+                a1 = fmax3(a1, s[x + 2], s[x + 3]);
+                a2 = fmax3(a2, s[x + 4], s[x + 5]);
+                a3 = fmax3(a3, s[x + 6], s[x + 7]);
+            }
+            a0 = fmax3(a0, s[124], s[125]);
+            a1 = fmax3(a1, s[126], s[127]);
+            const float m_cand = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3)) * scale2;
             if (j == 0) {
                 m_run = m_cand;
             } else {
@@ -242,7 +268,6 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
                 if (__any_sync(0xffffffffu, need)) {
                     const float m_new = fmaxf(m_run, m_cand);
                     const float alpha = ex2(m_run - m_new);
-                    h_run = alpha * (h_run + (m_run - m_new) * l_run);
                     l_run *= alpha;
                     m_run = m_new;
                     // O must hold every earlier P V product before it is rescaled
@@ -265,6 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
                 }
             }
             const float neg_m = -m_run;
+            float l0 = 0.f, l1 = 0.f, l2 = 0.f, l3 = 0.f;
 #pragma unroll
             for (int cc = 0; cc < 4; ++cc) {
                 uint32_t pk[16];
@@ -272,13 +298,17 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
                 for (int x = 0; x < 16; ++x) {
                     const float t0 = fmaf(s[cc * 32 + 2 * x], scale2, neg_m);
                     const float t1 = fmaf(s[cc * 32 + 2 * x + 1], scale2, neg_m);
-                    const float p0 = ex2(t0), p1 = ex2(t1);
-                    l_run += p0 + p1;
-                    h_run = fmaf(p0, t0, fmaf(p1, t1, h_run));
+                    // one pair in four goes through the FMA pipe: the MUFU pipe (16 ex2/clk/SM)
+                    // is the softmax's binding unit (SURVEY §7 hard part 4)
+                    const bool emu = (x & 3) == 3;
+                    const float p0 = emu ? ex2_emu(t0) : ex2(t0);
+                    const float p1 = emu ? ex2_emu(t1) : ex2(t1);
+                    if ((x & 1) == 0) { l0 += p0; l1 += p1; } else { l2 += p0; l3 += p1; }
                     pk[x] = pack_bf16(p0, p1);
                 }
                 VMB_TMEM_ST16(tS + cc * 16, pk);
             }
+            l_run += (l0 + l1) + (l2 + l3);
             tmem_st_wait();
             tc_fence_before();
             mbar_arrive(&p_full[j & 1]);
@@ -289,6 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
         tc_fence_after();
         const float inv_l = 1.f / l_run;
         const int64_t ob = u / a.oHn, oh = u % a.oHn;
+        float qo = 0.f;  // <q_row, sum_l p_l k_l>  (entropy, see below)
 #pragma unroll
         for (int t = 0; t < NO; ++t) {
             __nv_bfloat16* out = static_cast<__nv_bfloat16*>(t == 0 ? a.out0 : a.out1);
@@ -299,6 +330,20 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
                 uint32_t orr[32];
                 VMB_TMEM_LD32(tO + t * 128 + cc * 32 + lane_base, orr);
                 tmem_ld_wait();
+                if (t == 0 && a.cl_out) {
+                    // q row (bf16, SW128 panel cc/2) . O row, 32 columns
+                    const uint8_t* qp = smem + SM::q_off + (cc >> 1) * kPanelBytes;
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) {
+                        const uint4 qv = *reinterpret_cast<const uint4*>(qp + sw128_offset(row, (cc & 1) * 32 + 8 * x));
+                        const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            qo = fmaf(__uint_as_float(qw[e] << 16), __uint_as_float(orr[8 * x + 2 * e]), qo);
+                            qo = fmaf(__uint_as_float(qw[e] & 0xFFFF0000u), __uint_as_float(orr[8 * x + 2 * e + 1]), qo);
+                        }
+                    }
+                }
                 if (valid) {
                     uint4* dst = reinterpret_cast<uint4*>(orow + cc * 32);
 #pragma unroll
@@ -314,11 +359,14 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
             }
         }
         if (valid) {
-            const float ln_l = logf(l_run);
+            const float lse2 = m_run + log2f(l_run);  // base-2 log-sum-exp of x' = s * scale2
+            // sum_l R ln R = ln2 * (scale2 * sum_l R_l s_l - lse2), and in the R-step (value
+            // operand = the key tile) sum_l R_l s_l = <q, sum_l R_l k_l> = qo / l: the entropy
+            // of monarch.hpp:93-98 without a per-element accumulator.
             if (a.cl_out)
-                a.cl_out[((int64_t)u * a.q_len + grow) * a.nseg + seg] = kLn2 * h_run * inv_l - ln_l;
+                a.cl_out[((int64_t)u * a.q_len + grow) * a.nseg + seg] = kLn2 * (scale2 * qo * inv_l - lse2);
             if (a.lse_out)
-                a.lse_out[((int64_t)u * a.nseg + seg) * a.q_len + grow] = kLn2 * (m_run + log2f(l_run));
+                a.lse_out[((int64_t)u * a.nseg + seg) * a.q_len + grow] = kLn2 * lse2;
         }
     }
 
@@ -348,6 +396,8 @@ void launch(const Params& p, int64_t U, cudaStream_t s) {
 void tc_fa_launch(const TcFaArgs& a, int64_t U, cudaStream_t s) {
     if (U == 0 || a.q_len == 0) return;
     VMB_REQUIRE_DIM(a.kv_len >= 1, "attention over empty keys");
+    // the entropy output is derived from <q, P K>: the first value operand must be K
+    VMB_REQUIRE_DIM(!a.cl_out || a.nv == 2 || a.v_is_k, "entropy output needs the key tile as value operand");
     Params p;
     p.a = a;
     p.n_kv_tiles = (a.kv_len + kTile - 1) / kTile;

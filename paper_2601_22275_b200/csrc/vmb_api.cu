@@ -124,6 +124,7 @@ inline size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
 
 struct Shape {
     int64_t T, h, w, d, H, B, U, N, m, b, hw;
+    bool recompute;
 };
 
 Shape make_shape(const vmb_grid* g, const vmb_config* c) {
@@ -142,6 +143,7 @@ Shape make_shape(const vmb_grid* g, const vmb_config* c) {
     s.U = s.H * s.B;
     s.N = s.T * s.h * s.w;
     s.hw = s.h * s.w;
+    s.recompute = c->recompute_first_frame != 0;
     if (c->override_m != 0 || c->override_b != 0) {
         VMB_REQUIRE_DIM(c->override_m >= 1 && c->override_b >= 1 && c->override_m * c->override_b == s.N,
                         "override factor sizes must satisfy m*b = N");
@@ -161,6 +163,9 @@ struct Workspace {
     void* y;
     float* cR;
     float* cL;
+    float* part_o;    // split-KV partials of the first-frame recompute (tcgen05 path)
+    float* part_lse;
+    int nsplit;
     size_t bytes;
 };
 
@@ -177,6 +182,17 @@ Workspace carve(void* base, const Shape& s, vmb_dtype dt) {
     w.y = p + off; off += act;
     w.cR = reinterpret_cast<float*>(p + off); off += st;
     w.cL = reinterpret_cast<float*>(p + off); off += st;
+    w.part_o = w.part_lse = nullptr;
+    w.nsplit = 1;
+    if (dt == VMB_BF16 && s.d == 128 && s.recompute && s.U > 0) {
+        w.nsplit = tc2_plan_splits(s.hw, s.N, s.U, 2, kTc2MaxSplit);
+        if (w.nsplit > 1) {
+            w.part_o = reinterpret_cast<float*>(p + off);
+            off += align_up((size_t)s.U * w.nsplit * s.hw * 128 * sizeof(float));
+            w.part_lse = reinterpret_cast<float*>(p + off);
+            off += align_up((size_t)s.U * w.nsplit * s.hw * sizeof(float));
+        }
+    }
     w.bytes = off;
     return w;
 }
@@ -287,6 +303,7 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
         const CUtensorMap mQrow = user_map(q, in, s, b, 1, m, b, 128, 1);    // (d, i, k): query tiles
         const CUtensorMap mK = user_map(k, in, s, b, 1, m, b, 128, 1);
         const CUtensorMap mV = user_map(v, in, s, b, 1, m, b, 128, 1);
+        const CUtensorMap mK2 = user_map(k, in, s, b, 1, m, b, (uint32_t)tc2_kv_tile(1), 1);  // fa2 key tiles
         const uint32_t lrows = (uint32_t)lstep_rows(m);
         const CUtensorMap mQcol = user_map(q, in, s, b, 1, m, b, 1, lrows);   // (d, i, j): Qb[i] boxes
         const CUtensorMap mAR = internal_map(ws.aR, U, m, b, d, true, 128, 1);  // aR (U,m,b,d): (d,i,k) query tiles
@@ -320,7 +337,33 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
             fa.lse_out = nullptr;
             fa.status = ws.status;
             fa.check_finite = t == 0;
-            tc_fa_launch(fa, U, st);
+            if (last) {
+                tc_fa_launch(fa, U, st);
+            } else {
+                // R half-step without y: the 2-CTA/SM kernel (value operand = key tile)
+                Tc2Args f2{};
+                f2.tmQ = fa.tmQ;
+                f2.tmK = mK2;
+                f2.tmV = mK2;
+                f2.nseg = fa.nseg;
+                f2.q_len = fa.q_len;
+                f2.kv_len = fa.kv_len;
+                f2.qH = fa.qH;
+                f2.kH = fa.kH;
+                f2.oHn = 1;
+                f2.cR = fa.cR;
+                f2.qscale = fa.qscale;
+                f2.clamp_min = fa.clamp_min;
+                f2.clamp_enabled = fa.clamp_enabled;
+                f2.nv = 1;
+                f2.out = ws.aL;
+                f2.oB = b * m * d; f2.oH = 0; f2.oS = d; f2.oR = m * d;
+                f2.cl_out = ws.cL;
+                f2.status = ws.status;
+                f2.check_finite = fa.check_finite;
+                f2.max_split = 1;
+                tc2_fa_launch(f2, U, st);
+            }
 
             TcLstepArgs ls{};
             ls.tmQ = mQcol;
@@ -339,24 +382,26 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
             tc_lstep_launch(ls, U, st);
         }
         if (recompute) {
-            TcFaArgs fa{};
-            fa.tmQ = user_map(q, in, s, s.hw, 1, 1, s.hw, 128, 1);
-            fa.tmK = user_map(k, in, s, s.N, 1, 1, s.N, 128, 1);
-            fa.tmV = user_map(v, in, s, s.N, 1, 1, s.N, 128, 1);
-            fa.nseg = 1;
-            fa.q_len = (int32_t)s.hw;
-            fa.kv_len = (int32_t)s.N;
-            fa.qH = fa.kH = fa.oHn = (int32_t)std::max<int64_t>(s.H, 1);
-            fa.cR = nullptr;
-            fa.qscale = qscale;
-            fa.clamp_enabled = 0;
-            fa.clamp_min = 0.f;
-            fa.nv = 1;
-            fa.v_is_k = 0;
-            fa.out0 = o;
-            fa.oB[0] = out.batch; fa.oH[0] = out.head; fa.oS[0] = 0; fa.oR[0] = out.token;
-            fa.status = ws.status;
-            tc_fa_launch(fa, U, st);
+            // first-frame recompute: Q[0:hw) against all N keys, split over the keys
+            const int64_t Hm = std::max<int64_t>(s.H, 1);
+            const uint32_t bn = (uint32_t)tc2_kv_tile(2);
+            Tc2Args f2{};
+            f2.tmQ = user_map(q, in, s, s.hw, 1, 1, s.hw, 128, 1);
+            f2.tmK = user_map(k, in, s, s.N, 1, 1, s.N, bn, 1);
+            f2.tmV = user_map(v, in, s, s.N, 1, 1, s.N, bn, 1);
+            f2.nseg = 1;
+            f2.q_len = (int32_t)s.hw;
+            f2.kv_len = (int32_t)s.N;
+            f2.qH = f2.kH = f2.oHn = (int32_t)Hm;
+            f2.qscale = qscale;
+            f2.nv = 2;
+            f2.out = o;
+            f2.oB = out.batch; f2.oH = out.head; f2.oS = 0; f2.oR = out.token;
+            f2.status = ws.status;
+            f2.part_o = ws.part_o;
+            f2.part_lse = ws.part_lse;
+            f2.max_split = ws.part_o ? kTc2MaxSplit : 1;
+            tc2_fa_launch(f2, U, st);
         }
         return;
     }
@@ -622,28 +667,26 @@ vmb_status vmb_rstep(int64_t units, int64_t m, int64_t b, int64_t d, vmb_dtype d
         const bool tc = bf16 && d == 128 && R == nullptr && tmap_supported() && aligned16(aR) && aligned16(Kb) &&
                         aligned16(aL) && b <= INT32_MAX;
         if (tc) {
-            TcFaArgs fa{};
-            fa.tmQ = internal_map(aR, units, m, b, d, true, 128, 1);
-            fa.tmK = internal_map(Kb, units, m, b, d, true, 128, 1);
-            fa.tmV = fa.tmK;
-            fa.nseg = (int32_t)m;
-            fa.q_len = fa.kv_len = (int32_t)b;
-            fa.qH = fa.kH = fa.oHn = 1;
-            fa.cR = cR;
-            fa.qscale = 1.f;
-            fa.clamp_min = (float)clamp_min;
-            fa.clamp_enabled = clamp_enabled;
-            fa.nv = 1;
-            fa.v_is_k = 1;
-            fa.out0 = aL;
-            fa.oB[0] = b * m * d; fa.oH[0] = 0; fa.oS[0] = d; fa.oR[0] = m * d;
-            fa.cl_out = cL;
-            fa.status = nullptr;
-            fa.check_finite = 0;
+            Tc2Args f2{};
+            f2.tmQ = internal_map(aR, units, m, b, d, true, 128, 1);
+            f2.tmK = internal_map(Kb, units, m, b, d, true, (uint32_t)tc2_kv_tile(1), 1);
+            f2.tmV = f2.tmK;
+            f2.nseg = (int32_t)m;
+            f2.q_len = f2.kv_len = (int32_t)b;
+            f2.qH = f2.kH = f2.oHn = 1;
+            f2.cR = cR;
+            f2.qscale = 1.f;
+            f2.clamp_min = (float)clamp_min;
+            f2.clamp_enabled = clamp_enabled;
+            f2.nv = 1;
+            f2.out = aL;
+            f2.oB = b * m * d; f2.oH = 0; f2.oS = d; f2.oR = m * d;
+            f2.cl_out = cL;
+            f2.max_split = 1;
             int32_t* dummy = nullptr;
             VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dummy), sizeof(int32_t), st));
-            fa.status = dummy;
-            tc_fa_launch(fa, units, st);
+            f2.status = dummy;
+            tc2_fa_launch(f2, units, st);
             VMB_CHECK_CUDA(cudaFreeAsync(dummy, st));
             return;
         }
@@ -727,30 +770,43 @@ vmb_status vmb_flash_entropy_fwd(int64_t units, int64_t nq, int64_t nk, int64_t 
         const bool tc = bf16 && d == 128 && ent == nullptr && tmap_supported() && aligned16(q) && aligned16(k) &&
                         aligned16(v) && aligned16(o) && nq <= INT32_MAX && nk <= INT32_MAX;
         if (tc) {
-            TcFaArgs fa{};
+            Tc2Args f2{};
+            const uint32_t bn = (uint32_t)tc2_kv_tile(2);
             const uint64_t sq = (uint64_t)(nq * d * 2), sk = (uint64_t)(nk * d * 2);
             const uint64_t dq[5] = {(uint64_t)d, (uint64_t)nq, 1, 1, (uint64_t)std::max<int64_t>(units, 1)};
             const uint64_t dk[5] = {(uint64_t)d, (uint64_t)nk, 1, 1, (uint64_t)std::max<int64_t>(units, 1)};
             const uint64_t stq[4] = {(uint64_t)(d * 2), sq, sq, sq};
             const uint64_t stk[4] = {(uint64_t)(d * 2), sk, sk, sk};
-            const uint32_t box[5] = {64, 128, 1, 1, 1};
-            fa.tmQ = make_tmap_bf16_5d(q, dq, stq, box);
-            fa.tmK = make_tmap_bf16_5d(k, dk, stk, box);
-            fa.tmV = make_tmap_bf16_5d(v, dk, stk, box);
-            fa.nseg = 1;
-            fa.q_len = (int32_t)nq;
-            fa.kv_len = (int32_t)nk;
-            fa.qH = fa.kH = fa.oHn = 1;
-            fa.qscale = q_scale;
-            fa.nv = 1;
-            fa.v_is_k = 0;
-            fa.out0 = o;
-            fa.oB[0] = nq * d; fa.oH[0] = 0; fa.oS[0] = 0; fa.oR[0] = d;
-            fa.lse_out = lse;
+            const uint32_t boxq[5] = {64, 128, 1, 1, 1};
+            const uint32_t boxk[5] = {64, bn, 1, 1, 1};
+            f2.tmQ = make_tmap_bf16_5d(q, dq, stq, boxq);
+            f2.tmK = make_tmap_bf16_5d(k, dk, stk, boxk);
+            f2.tmV = make_tmap_bf16_5d(v, dk, stk, boxk);
+            f2.nseg = 1;
+            f2.q_len = (int32_t)nq;
+            f2.kv_len = (int32_t)nk;
+            f2.qH = f2.kH = f2.oHn = 1;
+            f2.qscale = q_scale;
+            f2.nv = 2;
+            f2.out = o;
+            f2.oB = nq * d; f2.oH = 0; f2.oS = 0; f2.oR = d;
+            f2.lse_out = lse;
+            const int nsplit = tc2_plan_splits(nq, nk, units, 2, kTc2MaxSplit);
+            float* part = nullptr;
             int32_t* dummy = nullptr;
             VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dummy), sizeof(int32_t), st));
-            fa.status = dummy;
-            tc_fa_launch(fa, units, st);
+            if (nsplit > 1) {
+                VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part),
+                                               (size_t)units * nsplit * nq * 129 * sizeof(float), st));
+                f2.part_o = part;
+                f2.part_lse = part + (size_t)units * nsplit * nq * 128;
+                f2.max_split = kTc2MaxSplit;
+            } else {
+                f2.max_split = 1;
+            }
+            f2.status = dummy;
+            tc2_fa_launch(f2, units, st);
+            if (part) VMB_CHECK_CUDA(cudaFreeAsync(part, st));
             VMB_CHECK_CUDA(cudaFreeAsync(dummy, st));
             return;
         }
