@@ -33,7 +33,7 @@ __all__ = [
     "kernel_launch_count", "LIB_PATH",
 ]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libvmb.so")
+LIB_PATH = os.environ.get("VMB_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libvmb.so")
 
 
 class DimensionError(ValueError):

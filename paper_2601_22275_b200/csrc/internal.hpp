@@ -180,6 +180,45 @@ int tc2_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg, int nv, int m
 // Largest split count tc2_fa_launch may pick (sizes the partial buffers).
 constexpr int kTc2MaxSplit = 16;
 void tc2_fa_launch(Tc2Args a, int64_t U, cudaStream_t s);
+// LSE combine of split-KV partials (a.nsplit, a.n_useg set by the launcher).
+void tc2_combine_launch(const Tc2Args& a, cudaStream_t s);
+// fa3_tc.cu: two 128-row query tiles per CTA, ping-pong softmax warpgroups, 128-key tiles
+// (K/V maps with box rows 128).  Same argument block as fa2.
+int tc3_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg, int max_split);
+void tc3_fa_launch(Tc2Args a, int64_t U, cudaStream_t s);
+// fa4_tc.cu: persistent (one CTA per SM) flash attention over a flattened stream of
+// (query tile, segment, kv-split) items; 128-key tiles (K/V maps with box rows 128).
+//   nv = 1, v_is_k = 1: R half-step (out0 = aL, cl_out)
+//   nv = 2            : R half-step + y (out0 = aL, out1 = y, cl_out), O = P [K | V]
+//   nv = 1, v_is_k = 0: attention (out0), optional split-KV (part_o / part_lse / max_split)
+struct Tc4Args {
+    CUtensorMap tmQ, tmK, tmV;   // 5-D maps (d, row, seg, head, batch)
+    int32_t nseg;
+    int32_t q_len, kv_len;
+    int32_t qH, kH, oHn;
+    const float* cR;
+    float qscale;
+    float clamp_min;
+    int32_t clamp_enabled;
+    int32_t nv;
+    int32_t v_is_k;
+    void* out0;
+    void* out1;
+    int64_t oB[2], oH[2], oS[2], oR[2];
+    float* cl_out;
+    float* lse_out;
+    int32_t* status;
+    int32_t check_finite;
+    float* part_o;
+    float* part_lse;
+    int32_t max_split;
+    int32_t nsplit;              // set by the launcher
+};
+int tc4_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg, int max_split);
+void tc4_fa_launch(Tc4Args a, int64_t U, cudaStream_t s);
+// Which attention kernel family serves a call: 2 = fa2 (R half-step default), 3 = fa3
+// (recompute / flash / dense default); env VMB_FA=2|3 forces one (A/B measurements).
+int attn_impl(bool rstep);
 
 // All L-step tiles are boxes of `rows = lstep_rows(m)` rows (m rounded up to 16); rows
 // >= m are OOB (zero-filled on load, clipped on store).

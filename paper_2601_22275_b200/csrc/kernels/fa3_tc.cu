@@ -1,5 +1,5 @@
-// fa2_tc.cu — tcgen05 flash attention with fused online statistics, two CTAs per SM
-// (bf16, d = 128, one value operand).
+// fa3_tc.cu — tcgen05 flash attention, two query tiles per CTA with ping-pong softmax
+// warpgroups (bf16, d = 128, one value operand).  The main attention kernel of the path.
 //
 // Serves:
 //   * the R half-step (monarch.hpp:53-103): query = aR[k] (or Q on the first step), key =
@@ -7,27 +7,30 @@
 //     outputs aL rows (strided into (b,m,d)) and cL = sum_l R ln R.                   <NB=1>
 //   * the first-frame recompute (flash_entropy.hpp:85-139, video.hpp:117-126) and the
 //     dense baseline (oracle.hpp:36-72): query = Q rows, key/value = all keys, split over
-//     the key axis (split-KV) with an LSE combine when the query tiles alone do not fill
-//     the machine.                                                                     <NB=2>
+//     the key axis with an LSE combine when the query tiles do not fill the machine. <NB=2>
 //
-// CTA = one 128-row query tile of one (unit, segment, kv-split).  192 threads:
-//   warp 0      TMA producer: Q tile once, then a ring of KV stages
-//   warp 1      TMEM allocator (256 columns) + single-thread tcgen05.mma issuer
-//   warps 2-5   softmax / statistics / epilogue; thread owns query row (warp%4)*32 + lane
-//               (TMEM lane restriction: warp w reaches lanes 32*(w%4) .. +31)
-// Key tiles of 64 (BN): TMEM holds two S buffers [0,64) and [64,128) (fp32; P written back
-// as bf16 over the first 32 columns of its buffer) and O [128, 256) -- 256 columns, so two
-// CTAs share an SM.  S_{j+1} is issued before the issuer waits for P_j (overlap inside the
-// CTA), and the SM's tensor pipe is shared by two CTAs whose softmax, prologue and epilogue
-// phases interleave (the FA4 ping-pong, across CTAs instead of warpgroups).  The softmax
-// uses packed FFMA2/FADD2 for x' - m and the row sum (half the FMA-pipe issue slots).
+// Why this shape (profiles/r1_micro_tcgen05.md): a tcgen05.mma costs >= ~80 cycles whatever
+// its N, so score tiles use N = 128 keys (N = 64 runs at half rate); the MUFU pipe gives 16
+// exp/clk/SM, i.e. a 128x128 score tile needs 1024 MUFU cycles against 1292 tensor cycles
+// for S + PV.  Two 128-row query tiles (A, B) share every K/V stage; while warpgroup A runs
+// the softmax of tile A the tensor pipe works on tile B and vice versa (FA4 ping-pong).
+//
+// CTA = query tiles (2p, 2p+1) of one (unit, segment, kv-split).  320 threads:
+//   warp 0      TMA producer: both Q tiles once, then a ring of K (or K,V) stages
+//   warp 1      TMEM allocator (512 columns) + single-thread tcgen05.mma issuer
+//   warps 2-5   softmax / epilogue of tile A, warps 6-9 of tile B; a thread owns query row
+//               (warp%4)*32 + lane (TMEM lane restriction: warp w reaches lanes 32*(w%4)..)
+// TMEM: tile t at column 256*t: S_t [0,128) fp32 (P_t written back as bf16 over its first
+// 64 columns), O_t [128, 256).
+// Issue order per key tile j:  PV_A(j), S_A(j+1), PV_B(j), S_B(j+1).  S_t(j+1) follows
+// PV_t(j) in the in-order tcgen05 pipeline, so (i) P_t(j) is consumed before S_t(j+1)
+// overwrites it and (ii) once a softmax warp sees S_t(j+1) complete, O_t holds every
+// earlier P V product -- the lazy O rescale needs no extra barrier.
 //
 // Statistics: base 2 with a lazily-updated reference max (O and l rescaled only when the
-// running max grows by more than 8).  The entropy of the R-step is not accumulated per
-// element: with value = key, sum_l R_l s_l = <q, sum_l R_l k_l> = <q, O> / l, so
+// running max grows by more than 8).  The R-step entropy uses value = key:
 //   sum_l R ln R = ln2 * (scale2 * <q, O> / l - lse2)            (monarch.hpp:93-98)
-// is one 128-term dot product in the epilogue.  A quarter of the exponentials run as a
-// degree-3 polynomial on the FMA pipe (MUFU ex2 is 16/clk/SM, the softmax's binding unit).
+// one 128-term dot product in the epilogue instead of a per-element accumulator.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -40,9 +43,11 @@ namespace {
 
 using namespace ptx;
 
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;
 constexpr int kQTile = 128;
-constexpr uint32_t kQPanel = 128 * 128;        // 128 rows x 64 bf16
+constexpr int kBN = 128;                        // keys per KV tile
+constexpr uint32_t kPanel = 128 * 128;          // 128 rows x 64 bf16 (SW128)
+constexpr uint32_t kTileBytes = 2 * kPanel;     // 128 x 128 bf16
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescaleThreshold = 8.0f;
@@ -53,28 +58,6 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
     asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
     return d;
 }
-// 2^x on the FMA/ALU pipes (see fa_tc.cu): rel. err 1.1e-4, far below the bf16 P rounding.
-__device__ __forceinline__ float ex2_emu(float x) {
-    x = fmaxf(x, -126.f);
-    const float kMagic = 12582912.f;
-    const float t = x + kMagic;
-    const float f = x - (t - kMagic);
-    const float p = fmaf(fmaf(fmaf(0.05592203512787819f, f, 0.24264007806777954f), f, 0.6931210160255432f), f,
-                         0.9999244809150696f);
-    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
-
-// packed variant of ex2_emu for an element pair (FADD2/FFMA2 + integer exponent add)
-__device__ __forceinline__ uint64_t ex2_emu2(uint64_t x2);
-
-struct Params {
-    Tc2Args a;
-    int32_t n_kv_tiles;   // key tiles per split (the last split may own fewer)
-    int32_t total_tiles;  // key tiles of the whole segment
-    int32_t q_tiles;
-};
-
-// packed fp32 pair arithmetic (FFMA2 / FADD2, sm_100)
 __device__ __forceinline__ uint64_t ffma2(uint64_t x, uint64_t b, uint64_t c) {
     uint64_t d;
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(x), "l"(b), "l"(c));
@@ -90,13 +73,13 @@ __device__ __forceinline__ uint64_t pk2(float lo, float hi) {
 }
 __device__ __forceinline__ float lo2(uint64_t v) { return __uint_as_float((uint32_t)v); }
 __device__ __forceinline__ float hi2(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
-
+// 2^x for an element pair on the FMA/ALU pipes: n = rint(x) via the 1.5*2^23 magic, 2^(x-n)
+// by a degree-3 minimax polynomial on [-0.5, 0.5] (rel. err 1.1e-4, far below the bf16 P
+// rounding), n added to the exponent field; x clamped at -126.
 __device__ __forceinline__ uint64_t ex2_emu2(uint64_t x2) {
-    const float x0 = fmaxf(lo2(x2), -126.f), x1 = fmaxf(hi2(x2), -126.f);
-    const uint64_t xx = pk2(x0, x1);
-    const uint64_t magic = pk2(12582912.f, 12582912.f), nmagic = pk2(-12582912.f, -12582912.f);
-    const uint64_t t = fadd2(xx, magic);
-    const uint64_t f = fadd2(xx, fadd2(nmagic, t) ^ 0x8000000080000000ull);  // x - (t - magic)
+    const uint64_t xx = pk2(fmaxf(lo2(x2), -126.f), fmaxf(hi2(x2), -126.f));
+    const uint64_t t = fadd2(xx, pk2(12582912.f, 12582912.f));
+    const uint64_t f = fadd2(xx, fadd2(pk2(-12582912.f, -12582912.f), t) ^ 0x8000000080000000ull);
     uint64_t p = ffma2(pk2(0.05592203512787819f, 0.05592203512787819f), f,
                        pk2(0.24264007806777954f, 0.24264007806777954f));
     p = ffma2(p, f, pk2(0.6931210160255432f, 0.6931210160255432f));
@@ -106,25 +89,28 @@ __device__ __forceinline__ uint64_t ex2_emu2(uint64_t x2) {
     return (uint64_t)r0 | ((uint64_t)r1 << 32);
 }
 
-constexpr int kBN = 64;  // keys per KV tile (S tile = 128 x 64, double-buffered in TMEM)
+struct Params {
+    Tc2Args a;
+    int32_t n_kv_tiles;   // key tiles per split (the last split may own fewer)
+    int32_t total_tiles;  // key tiles of the whole segment
+    int32_t q_pairs;      // CTAs (tile pairs) per segment
+};
 
 template <int NB>
 struct Smem {
-    static constexpr int S = NB == 1 ? 4 : 2;             // KV stages
-    static constexpr uint32_t kv_panel = kBN * 128;       // 64 rows x 64 bf16
-    static constexpr uint32_t kv_tile = 2 * kv_panel;     // 64 x 128
-    static constexpr uint32_t q_off = 0;
-    static constexpr uint32_t kv_off = 2 * kQPanel;
-    static constexpr uint32_t bar_off = kv_off + S * NB * kv_tile;
-    // q_full, kv_full[S], kv_empty[S], s_full[2], p_full[2], pv_done, o_full
-    static constexpr uint32_t n_bars = 1 + 2 * S + 6;
+    static constexpr int S = NB == 1 ? 3 : 2;              // KV stages
+    static constexpr uint32_t q_off = 0;                   // Q_A, Q_B
+    static constexpr uint32_t kv_off = 2 * kTileBytes;
+    static constexpr uint32_t bar_off = kv_off + S * NB * kTileBytes;
+    // q_full, kv_full[S], kv_empty[S], s_full[2], p_full[2], o_full
+    static constexpr uint32_t n_bars = 1 + 2 * S + 5;
     static constexpr uint32_t slot_off = bar_off + n_bars * 8;
     static constexpr uint32_t bytes = slot_off + 16;
     static constexpr uint32_t alloc = bytes + 1024;
 };
 
 template <int NB>
-__global__ void __launch_bounds__(kThreads, 2) fa2_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(kThreads, 1) fa3_kernel(const __grid_constant__ Params p) {
     using SM = Smem<NB>;
     constexpr int S = SM::S;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -133,16 +119,15 @@ __global__ void __launch_bounds__(kThreads, 2) fa2_kernel(const __grid_constant_
     uint64_t* q_full = bars;
     uint64_t* kv_full = bars + 1;
     uint64_t* kv_empty = bars + 1 + S;
-    uint64_t* s_full = bars + 1 + 2 * S;   // [2]
-    uint64_t* p_full = s_full + 2;         // [2]
-    uint64_t* pv_done = s_full + 4;
-    uint64_t* o_full = s_full + 5;
+    uint64_t* s_full = bars + 1 + 2 * S;  // [2]
+    uint64_t* p_full = s_full + 2;        // [2]
+    uint64_t* o_full = s_full + 4;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM::slot_off);
 
     const Tc2Args& a = p.a;
     const int warp = warp_id();
-    const int qtile = blockIdx.x % p.q_tiles;
-    const int split = blockIdx.x / p.q_tiles;
+    const int pair = blockIdx.x % p.q_pairs;
+    const int split = blockIdx.x / p.q_pairs;
     const int useg = blockIdx.y;  // u * nseg + seg
     const int u = useg / a.nseg, seg = useg % a.nseg;
     const int kv_tile0 = split * p.n_kv_tiles;
@@ -157,20 +142,18 @@ __global__ void __launch_bounds__(kThreads, 2) fa2_kernel(const __grid_constant_
             mbar_init(&kv_full[s], 1);
             mbar_init(&kv_empty[s], 1);
         }
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(&s_full[s], 1);
-            mbar_init(&p_full[s], 128);
+        for (int t = 0; t < 2; ++t) {
+            mbar_init(&s_full[t], 1);
+            mbar_init(&p_full[t], 128);
         }
-        mbar_init(pv_done, 1);
         mbar_init(o_full, 1);
         fence_mbar_init();
     }
-    if (warp == 1) tmem_alloc<256>(tmem_slot);
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t tS0 = tmem, tO = tmem + 128;   // S buffers at [0,64) and [64,128)
 
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer
@@ -178,69 +161,84 @@ __global__ void __launch_bounds__(kThreads, 2) fa2_kernel(const __grid_constant_
             const int qb = u / a.qH, qh = u % a.qH;
             const int kb = u / a.kH, kh = u % a.kH;
             uint8_t* sq = smem + SM::q_off;
-            mbar_arrive_expect_tx(q_full, 2 * kQPanel);
-            tma_load_5d(sq, &a.tmQ, q_full, 0, qtile * kQTile, seg, qh, qb);
-            tma_load_5d(sq + kQPanel, &a.tmQ, q_full, 64, qtile * kQTile, seg, qh, qb);
+            mbar_arrive_expect_tx(q_full, 2 * kTileBytes);
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                const int row = (2 * pair + t) * kQTile;
+                tma_load_5d(sq + t * kTileBytes, &a.tmQ, q_full, 0, row, seg, qh, qb);
+                tma_load_5d(sq + t * kTileBytes + kPanel, &a.tmQ, q_full, 64, row, seg, qh, qb);
+            }
             for (int j = 0; j < n_kv; ++j) {
                 const int st = j % S;
                 if (j >= S) mbar_wait_sleep(&kv_empty[st], ((j / S) + 1) & 1);
-                uint8_t* skv = smem + SM::kv_off + st * NB * SM::kv_tile;
+                uint8_t* skv = smem + SM::kv_off + st * NB * kTileBytes;
                 const int row = (kv_tile0 + j) * kBN;
-                mbar_arrive_expect_tx(&kv_full[st], NB * SM::kv_tile);
+                mbar_arrive_expect_tx(&kv_full[st], NB * kTileBytes);
                 tma_load_5d(skv, &a.tmK, &kv_full[st], 0, row, seg, kh, kb);
-                tma_load_5d(skv + SM::kv_panel, &a.tmK, &kv_full[st], 64, row, seg, kh, kb);
+                tma_load_5d(skv + kPanel, &a.tmK, &kv_full[st], 64, row, seg, kh, kb);
                 if (NB == 2) {
-                    tma_load_5d(skv + SM::kv_tile, &a.tmV, &kv_full[st], 0, row, seg, kh, kb);
-                    tma_load_5d(skv + SM::kv_tile + SM::kv_panel, &a.tmV, &kv_full[st], 64, row, seg, kh, kb);
+                    tma_load_5d(skv + kTileBytes, &a.tmV, &kv_full[st], 0, row, seg, kh, kb);
+                    tma_load_5d(skv + kTileBytes + kPanel, &a.tmV, &kv_full[st], 64, row, seg, kh, kb);
                 }
             }
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        // S_j = Q K_j^T into buffer j&1 is issued before waiting for P_{j-1}, so the tensor
-        // pipe computes the next score tile while the softmax warps work on the current one.
         constexpr uint32_t idS = idesc_bf16(128, kBN, 0, 0);   // S = Q K^T, both K-major
         constexpr uint32_t idPV = idesc_bf16(128, 128, 0, 1);  // O += P V, V MN-major
         const uint32_t q_addr = smem_u32(smem + SM::q_off);
         const uint32_t kv_addr = smem_u32(smem + SM::kv_off);
         if (elect_one()) {
+            auto issue_s = [&](int t, int j) {
+                const uint32_t kaddr = kv_addr + (j % S) * NB * kTileBytes;
+                const uint32_t qa = q_addr + t * kTileBytes;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t off = (kk >> 2) * kPanel + (kk & 3) * 32;
+                    umma_ss(tmem + t * 256, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(kaddr + off, 16, 1024), idS,
+                            kk > 0);
+                }
+                umma_commit(&s_full[t]);
+            };
+            auto issue_pv = [&](int t, int j) {
+                const uint32_t vaddr = kv_addr + (j % S) * NB * kTileBytes + (NB == 2 ? kTileBytes : 0);
+#pragma unroll
+                for (int kk = 0; kk < kBN / 16; ++kk)
+                    umma_ts(tmem + t * 256 + 128, tmem + t * 256 + kk * 8, sdesc_sw128(vaddr + kk * 2048, kPanel, 1024),
+                            idPV, (j > 0 || kk > 0) ? 1u : 0u);
+            };
             mbar_wait_sleep(q_full, 0);
-            for (int j = 0; j <= n_kv; ++j) {
-                if (j < n_kv) {
-                    const int st = j % S;
-                    mbar_wait_sleep(&kv_full[st], (j / S) & 1);
+            mbar_wait_sleep(&kv_full[0], 0);
+            tc_fence_after();
+            issue_s(0, 0);
+            issue_s(1, 0);
+            for (int j = 0; j < n_kv; ++j) {
+                const bool more = j + 1 < n_kv;
+                // tile A
+                mbar_wait_sleep(&p_full[0], j & 1);
+                tc_fence_after();
+                issue_pv(0, j);
+                if (more) {
+                    mbar_wait_sleep(&kv_full[(j + 1) % S], ((j + 1) / S) & 1);
                     tc_fence_after();
-                    const uint32_t kaddr = kv_addr + st * NB * SM::kv_tile;
-                    const uint32_t tS = tS0 + (j & 1) * kBN;
-#pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) {
-                        umma_ss(tS, sdesc_sw128(q_addr + (kk >> 2) * kQPanel + (kk & 3) * 32, 16, 1024),
-                                sdesc_sw128(kaddr + (kk >> 2) * SM::kv_panel + (kk & 3) * 32, 16, 1024), idS, kk > 0);
-                    }
-                    umma_commit(&s_full[j & 1]);
+                    issue_s(0, j + 1);
                 }
-                if (j >= 1) {
-                    const int jp = j - 1, st = jp % S;
-                    mbar_wait_sleep(&p_full[jp & 1], (jp >> 1) & 1);
-                    tc_fence_after();
-                    const uint32_t vaddr = kv_addr + st * NB * SM::kv_tile + (NB == 2 ? SM::kv_tile : 0);
-                    const uint32_t tP = tS0 + (jp & 1) * kBN;
-#pragma unroll
-                    for (int kk = 0; kk < kBN / 16; ++kk) {
-                        umma_ts(tO, tP + kk * 8, sdesc_sw128(vaddr + kk * 2048, SM::kv_panel, 1024), idPV,
-                                (jp > 0 || kk > 0) ? 1u : 0u);
-                    }
-                    umma_commit(&kv_empty[st]);
-                    umma_commit(pv_done);
-                }
+                // tile B
+                mbar_wait_sleep(&p_full[1], j & 1);
+                tc_fence_after();
+                issue_pv(1, j);
+                umma_commit(&kv_empty[j % S]);
+                if (more) issue_s(1, j + 1);
             }
             umma_commit(o_full);
         }
     } else {
         // ------------------------------------------------------------ softmax / epilogue
+        const int t = (warp - 2) >> 2;                // query tile of this warpgroup
         const int row = (warp & 3) * 32 + lane_id();  // TMEM lane == query row in tile
         const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-        const int grow = qtile * kQTile + row;        // row within the segment
+        const uint32_t tS = tmem + t * 256 + lane_base, tO = tS + 128;
+        const int grow = (2 * pair + t) * kQTile + row;  // row within the segment
         const bool valid = grow < a.q_len;
         float c = 1.f;
         if (a.cR && valid) c = a.cR[((int64_t)u * a.nseg + seg) * a.q_len + grow];
@@ -254,13 +252,14 @@ __global__ void __launch_bounds__(kThreads, 2) fa2_kernel(const __grid_constant_
         // valid keys in this CTA's last tile (only the globally last tile is ragged)
         const int kv_end = (kv_tile0 + n_kv) * kBN;
         const int last_valid = kBN - (kv_end > a.kv_len ? kv_end - a.kv_len : 0);
+        const uint8_t* qtile_smem = smem + SM::q_off + t * kTileBytes;
 
         if (a.check_finite) {
             mbar_wait_sleep(q_full, 0);
             bool bad = false;
 #pragma unroll
             for (int pnl = 0; pnl < 2; ++pnl) {
-                const uint4* q4 = reinterpret_cast<const uint4*>(smem + SM::q_off + pnl * kQPanel + row * 128);
+                const uint4* q4 = reinterpret_cast<const uint4*>(qtile_smem + pnl * kPanel + row * 128);
 #pragma unroll
                 for (int x = 0; x < 8; ++x) {
                     const uint4 v = q4[x ^ (row & 7)];  // rotate chunks across lanes: no bank conflicts
@@ -276,22 +275,21 @@ __global__ void __launch_bounds__(kThreads, 2) fa2_kernel(const __grid_constant_
         float m_run = -INFINITY, l_run = 0.f;
         const uint64_t scale2x2 = pk2(scale2, scale2);
         for (int j = 0; j < n_kv; ++j) {
-            const uint32_t tS = tS0 + (j & 1) * kBN + lane_base;
-            mbar_wait_sleep(&s_full[j & 1], (j >> 1) & 1);
+            mbar_wait_sleep(&s_full[t], j & 1);
             tc_fence_after();
 #if VMB_DEBUG_NO_SOFTMAX  // timing experiment only: MMA/TMA pipeline without the softmax
             if (true) {
-                mbar_arrive(&p_full[j & 1]);
+                mbar_arrive(&p_full[t]);
                 continue;
             }
 #endif
             uint32_t sr[kBN];
-            VMB_TMEM_LD32(tS + 0, (sr + 0));
-            VMB_TMEM_LD32(tS + 32, (sr + 32));
+#pragma unroll
+            for (int cc = 0; cc < kBN / 32; ++cc) VMB_TMEM_LD32(tS + cc * 32, (sr + cc * 32));
             tmem_ld_wait();
             float* s = reinterpret_cast<float*>(sr);
             if (j == n_kv - 1 && last_valid < kBN) {
-                asm volatile("");  // keep this a real (rarely taken) branch, not 64 selects
+                asm volatile("");  // keep this a real (rarely taken) branch, not 128 selects
 #pragma unroll
                 for (int x = 0; x < kBN; ++x)
                     if (x >= last_valid) s[x] = kMasked;
@@ -308,7 +306,6 @@ __global__ void __launch_bounds__(kThreads, 2) fa2_kernel(const __grid_constant_
             a0 = fmax3(a0, s[kBN - 4], s[kBN - 3]);
             a1 = fmax3(a1, s[kBN - 2], s[kBN - 1]);
             const float m_cand = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3)) * scale2;
-            // lazy rescale decision; O itself is rescaled after P is stored (s[] dead by then)
             bool rescale = false;
             float alpha = 1.f;
             if (j == 0) {
@@ -323,49 +320,47 @@ __global__ void __launch_bounds__(kThreads, 2) fa2_kernel(const __grid_constant_
                     rescale = true;
                 }
             }
-            // x' - m for element pairs on the packed FMA pipe, then 2^(x' - m): MUFU for 7 of
-            // every 8 pairs, the FMA-pipe polynomial for the 8th
+            // x' - m on the packed FMA pipe, 2^(x' - m): MUFU for 7 of 8 pairs, FMA-pipe
+            // polynomial for the 8th; row sum in packed adds; P -> TMEM as bf16
             const uint64_t negm2 = pk2(-m_run, -m_run);
             const uint64_t* s2 = reinterpret_cast<const uint64_t*>(sr);
             uint64_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
-            uint32_t pk[kBN / 2];
 #pragma unroll
-            for (int x = 0; x < kBN / 2; ++x) {
-                const uint64_t t2 = ffma2(s2[x], scale2x2, negm2);
-                uint64_t pp;
-                if ((x % VMB_EMU_PERIOD) == VMB_EMU_PERIOD - 1) pp = ex2_emu2(t2);
-                else pp = pk2(ex2(lo2(t2)), ex2(hi2(t2)));
-                const float p0 = lo2(pp), p1 = hi2(pp);
-                switch (x & 3) {
-                    case 0: acc0 = fadd2(acc0, pp); break;
-                    case 1: acc1 = fadd2(acc1, pp); break;
-                    case 2: acc2 = fadd2(acc2, pp); break;
-                    default: acc3 = fadd2(acc3, pp); break;
+            for (int cc = 0; cc < kBN / 32; ++cc) {
+                uint32_t pk[16];
+#pragma unroll
+                for (int x = 0; x < 16; ++x) {
+                    const uint64_t t2 = ffma2(s2[cc * 16 + x], scale2x2, negm2);
+                    uint64_t pp;
+                    if ((x % VMB_EMU_PERIOD) == VMB_EMU_PERIOD - 1) pp = ex2_emu2(t2);
+                    else pp = pk2(ex2(lo2(t2)), ex2(hi2(t2)));
+                    switch (x & 3) {
+                        case 0: acc0 = fadd2(acc0, pp); break;
+                        case 1: acc1 = fadd2(acc1, pp); break;
+                        case 2: acc2 = fadd2(acc2, pp); break;
+                        default: acc3 = fadd2(acc3, pp); break;
+                    }
+                    pk[x] = pack_bf16(lo2(pp), hi2(pp));
                 }
-                pk[x] = pack_bf16(p0, p1);
+                VMB_TMEM_ST16(tS + cc * 16, pk);
             }
-            VMB_TMEM_ST16(tS + 0, (pk + 0));
-            VMB_TMEM_ST16(tS + 16, (pk + 16));
             const uint64_t acc = fadd2(fadd2(acc0, acc1), fadd2(acc2, acc3));
             l_run += lo2(acc) + hi2(acc);
             if (rescale) {
-                // O must hold P_{j-1} V_{j-1} before it is rescaled; P_j V_j waits for p_full
-                mbar_wait_sleep(pv_done, (j - 1) & 1);
-                tc_fence_after();
+                // S_t(j) was issued after PV_t(j-1): O_t is complete here
 #pragma unroll
                 for (int cc = 0; cc < 4; ++cc) {
                     uint32_t orr[32];
-                    const uint32_t ta = tO + cc * 32 + lane_base;
-                    VMB_TMEM_LD32(ta, orr);
+                    VMB_TMEM_LD32(tO + cc * 32, orr);
                     tmem_ld_wait();
 #pragma unroll
                     for (int x = 0; x < 32; ++x) orr[x] = __float_as_uint(__uint_as_float(orr[x]) * alpha);
-                    VMB_TMEM_ST32(ta, orr);
+                    VMB_TMEM_ST32(tO + cc * 32, orr);
                 }
             }
             tmem_st_wait();
             tc_fence_before();
-            mbar_arrive(&p_full[j & 1]);
+            mbar_arrive(&p_full[t]);
         }
 
         // ------------------------------------------------------------ epilogue
@@ -373,14 +368,13 @@ __global__ void __launch_bounds__(kThreads, 2) fa2_kernel(const __grid_constant_
         tc_fence_after();
         const float inv_l = 1.f / l_run;
         const float lse2 = m_run + log2f(l_run);  // base-2 log-sum-exp of x' = s * scale2
-        float qo = 0.f;                            // <q_row, O_row> (R-step entropy)
         if (a.part_o) {
             // split-KV partial: normalised fp32 O and natural-log lse of this split
             float* prow = a.part_o + (((int64_t)useg * a.nsplit + split) * a.q_len + grow) * 128;
 #pragma unroll
             for (int cc = 0; cc < 4; ++cc) {
                 uint32_t orr[32];
-                VMB_TMEM_LD32(tO + cc * 32 + lane_base, orr);
+                VMB_TMEM_LD32(tO + cc * 32, orr);
                 tmem_ld_wait();
                 if (valid) {
                     float4* dst = reinterpret_cast<float4*>(prow + cc * 32);
@@ -392,16 +386,17 @@ __global__ void __launch_bounds__(kThreads, 2) fa2_kernel(const __grid_constant_
             }
             if (valid) a.part_lse[((int64_t)useg * a.nsplit + split) * a.q_len + grow] = kLn2 * lse2;
         } else {
+            float qo = 0.f;  // <q_row, O_row> (R-step entropy)
             const int64_t ob = u / a.oHn, oh = u % a.oHn;
             __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(a.out) + ob * a.oB + oh * a.oH + (int64_t)seg * a.oS +
                                   (int64_t)grow * a.oR;
 #pragma unroll
             for (int cc = 0; cc < 4; ++cc) {
                 uint32_t orr[32];
-                VMB_TMEM_LD32(tO + cc * 32 + lane_base, orr);
+                VMB_TMEM_LD32(tO + cc * 32, orr);
                 tmem_ld_wait();
                 if (a.cl_out) {
-                    const uint8_t* qp = smem + SM::q_off + (cc >> 1) * kQPanel;
+                    const uint8_t* qp = qtile_smem + (cc >> 1) * kPanel;
 #pragma unroll
                     for (int x = 0; x < 4; ++x) {
                         const uint4 qv = *reinterpret_cast<const uint4*>(qp + sw128_offset(row, (cc & 1) * 32 + 8 * x));
@@ -438,82 +433,44 @@ __global__ void __launch_bounds__(kThreads, 2) fa2_kernel(const __grid_constant_
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc<256>(tmem);
+        tmem_dealloc<512>(tmem);
     }
-}
-
-// ---------------------------------------------------------------- split-KV combine
-// O[r] = sum_s w_s O_s / sum_s w_s, w_s = exp(lse_s - max lse): one warp per row.
-__global__ void __launch_bounds__(256) fa2_combine_kernel(const Tc2Args a) {
-    const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    const int64_t rows = (int64_t)a.q_len;
-    const int64_t useg = gw / rows, r = gw % rows;
-    if (useg >= a.n_useg) return;
-    const int u = (int)(useg / a.nseg), seg = (int)(useg % a.nseg);
-    const float* lse = a.part_lse + (useg * a.nsplit) * rows + r;
-    float mx = -INFINITY;
-    for (int s = 0; s < a.nsplit; ++s) mx = fmaxf(mx, lse[(int64_t)s * rows]);
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    float wsum = 0.f;
-    for (int s = 0; s < a.nsplit; ++s) {
-        const float w = __expf(lse[(int64_t)s * rows] - mx);
-        wsum += w;
-        const float4 v = reinterpret_cast<const float4*>(a.part_o + ((useg * a.nsplit + s) * rows + r) * 128)[lane];
-        acc.x = fmaf(w, v.x, acc.x);
-        acc.y = fmaf(w, v.y, acc.y);
-        acc.z = fmaf(w, v.z, acc.z);
-        acc.w = fmaf(w, v.w, acc.w);
-    }
-    const float inv = 1.f / wsum;
-    const int64_t ob = u / a.oHn, oh = u % a.oHn;
-    __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(a.out) + ob * a.oB + oh * a.oH + (int64_t)seg * a.oS + r * a.oR;
-    uint2 v;
-    v.x = pack_bf16(acc.x * inv, acc.y * inv);
-    v.y = pack_bf16(acc.z * inv, acc.w * inv);
-    reinterpret_cast<uint2*>(orow)[lane] = v;
-    if (a.lse_out && lane == 0) a.lse_out[useg * rows + r] = mx + logf(wsum);
 }
 
 template <int NB>
 void launch(const Params& p, int64_t n_useg, int nsplit, cudaStream_t s) {
     using SM = Smem<NB>;
-    auto kern = fa2_kernel<NB>;
+    auto kern = fa3_kernel<NB>;
     VMB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM::alloc));
-    dim3 grid((unsigned)(p.q_tiles * nsplit), (unsigned)n_useg);
+    dim3 grid((unsigned)(p.q_pairs * nsplit), (unsigned)n_useg);
     ProfScope ps(NB == 1 ? kKRstep : kKAttn, s);
     kern<<<grid, kThreads, SM::alloc, s>>>(p);
     count_launch();
-    check_launch("fa2_tc");
+    check_launch("fa3_tc");
 }
 
 }  // namespace
 
-int tc2_kv_tile(int) { return kBN; }
-
-int tc2_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg, int nv, int max_split) {
+int tc3_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg, int max_split) {
     if (max_split <= 1 || q_len <= 0 || n_useg <= 0) return 1;
-    const int64_t BN = tc2_kv_tile(nv);
-    const int64_t total_tiles = (kv_len + BN - 1) / BN;
-    // enough CTAs for ~8 waves of 2 CTAs per SM, and at least 8 key tiles per split
-    const int64_t base = ((q_len + kQTile - 1) / kQTile) * n_useg;
-    const int64_t want = (8 * 2 * 148 + base - 1) / base;
+    const int64_t total_tiles = (kv_len + kBN - 1) / kBN;
+    // ~8 waves of one CTA per SM, at least 8 key tiles per split
+    const int64_t base = ((q_len + 2 * kQTile - 1) / (2 * kQTile)) * n_useg;
+    const int64_t want = (8 * 148 + base - 1) / base;
     int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>({want, (int64_t)max_split, total_tiles / 8}));
-    // no empty splits
     while (nsplit > 1 && ((total_tiles + nsplit - 1) / nsplit) * (nsplit - 1) >= total_tiles) --nsplit;
     return nsplit;
 }
 
-void tc2_fa_launch(Tc2Args a, int64_t U, cudaStream_t s) {
+void tc3_fa_launch(Tc2Args a, int64_t U, cudaStream_t s) {
     if (U == 0 || a.q_len == 0) return;
     VMB_REQUIRE_DIM(a.kv_len >= 1, "attention over empty keys");
     VMB_REQUIRE_DIM(!a.cl_out || a.nv == 1, "entropy output needs the key tile as value operand");
-    const int BN = tc2_kv_tile(a.nv);
     Params p;
-    p.q_tiles = (a.q_len + kQTile - 1) / kQTile;
-    const int total_tiles = (a.kv_len + BN - 1) / BN;
+    p.q_pairs = (a.q_len + 2 * kQTile - 1) / (2 * kQTile);
+    const int total_tiles = (a.kv_len + kBN - 1) / kBN;
     const int64_t n_useg = U * a.nseg;
-    const int nsplit = a.part_o ? tc2_plan_splits(a.q_len, a.kv_len, n_useg, a.nv, a.max_split) : 1;
+    const int nsplit = a.part_o ? tc3_plan_splits(a.q_len, a.kv_len, n_useg, a.max_split) : 1;
     p.n_kv_tiles = (total_tiles + nsplit - 1) / nsplit;
     p.total_tiles = total_tiles;
     a.nsplit = nsplit;
@@ -523,14 +480,6 @@ void tc2_fa_launch(Tc2Args a, int64_t U, cudaStream_t s) {
     if (a.nv == 1) launch<1>(p, n_useg, nsplit, s);
     else launch<2>(p, n_useg, nsplit, s);
     if (nsplit > 1) tc2_combine_launch(p.a, s);
-}
-
-void tc2_combine_launch(const Tc2Args& a, cudaStream_t s) {
-    const int64_t warps = a.n_useg * a.q_len;
-    ProfScope ps(kKCombine, s);
-    fa2_combine_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(a);
-    count_launch();
-    check_launch("fa2_combine");
 }
 
 }  // namespace vmb

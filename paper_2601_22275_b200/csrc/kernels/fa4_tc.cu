@@ -1,0 +1,558 @@
+// fa4_tc.cu — persistent tcgen05 flash attention with fused online statistics (bf16, d = 128).
+//
+// One CTA per SM loops over work items (128-row query tile, unit*segment, kv-split); the
+// key/value tiles of consecutive items form one continuous stream through the TMA ring, so
+// an item's prologue (Q load, first S MMAs) and epilogue (O read-out, output stores)
+// overlap its neighbours' main loops.  This is what the short rows of the R half-step need
+// (12 key tiles per item at C4): a non-persistent CTA spends a third of its life in
+// prologue/epilogue latency.
+//
+// Modes:
+//   <NB=1, NO=1>  R half-step (monarch.hpp:53-103): value = key; outputs aL, cL
+//   <NB=2, NO=2>  last R half-step with y = R V fused (monarch.hpp:182-185): O = P [K | V],
+//                 one N = 256 MMA per k-step (the full-rate tcgen05 shape,
+//                 profiles/r1_micro_tcgen05.md)
+//   <NB=2, NO=1>  attention: first-frame recompute / dense baseline (flash_entropy.hpp:85-139)
+//
+// Warp roles (384 threads): warp 0 TMA producer, warp 1 TMEM allocator + single-thread MMA
+// issuer, warps 4-11 softmax + epilogue in two warpgroups that split every score row: the
+// thread of warpgroup h owns columns [64h, 64h+64) of query row (warp%4)*32 + lane (TMEM
+// lane restriction).  Two softmax warps per SM sub-partition keep the MUFU pipe fed (one
+// warp alone is dependency-bound); the row max / sum / entropy partials meet in shared
+// memory (one named barrier per key tile).
+// TMEM (512 columns): S0 [0,128), S1 [128,256) double-buffered scores (P written back as
+// bf16 over the first 64 columns); NO=1: O0 [256,384), O1 [384,512) double-buffered over
+// items; NO=2: O [256,512) = [P K | P V].
+// Shared memory: Q double-buffered over items (2 x 32 KB) + the K (or K|V) ring.
+//
+// Issue order (flattened tile index g over this CTA's items): S(g), PV(g-1), S(g+1), ...
+// S(g) goes to buffer g&1 after PV(g-2) has been issued (in-order tcgen05 pipeline), and
+// an item's first PV waits for the epilogue to have drained that O buffer (o_empty).
+//
+// Statistics: base 2, lazily rescaled reference max (threshold 8).  With value = key the
+// entropy is  sum_l R ln R = ln2 * (scale2 * <q, O_K> / l - lse2)  (monarch.hpp:93-98): one
+// dot product in the epilogue.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "../internal.hpp"
+#include "sm100_ptx.cuh"
+
+namespace vmb {
+namespace {
+
+using namespace ptx;
+
+constexpr int kThreads = 384;
+constexpr int kTile = 128;                      // query rows per item, keys per KV tile
+constexpr uint32_t kPanel = 128 * 128;          // 128 rows x 64 bf16 (SW128)
+constexpr uint32_t kTileBytes = 2 * kPanel;     // 128 x 128 bf16
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kRescaleThreshold = 8.0f;
+constexpr float kMasked = -1.0e30f;
+
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t x, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(x), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t x, uint64_t y) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(x), "l"(y));
+    return d;
+}
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+    return (uint64_t)__float_as_uint(lo) | ((uint64_t)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ float lo2(uint64_t v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float hi2(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+// 2^x for an element pair on the FMA/ALU pipes (degree-3 minimax on [-0.5,0.5], rel. err
+// 1.1e-4; see fa3_tc.cu)
+__device__ __forceinline__ uint64_t ex2_emu2(uint64_t x2) {
+    const uint64_t xx = pk2(fmaxf(lo2(x2), -126.f), fmaxf(hi2(x2), -126.f));
+    const uint64_t t = fadd2(xx, pk2(12582912.f, 12582912.f));
+    const uint64_t f = fadd2(xx, fadd2(pk2(-12582912.f, -12582912.f), t) ^ 0x8000000080000000ull);
+    uint64_t p = ffma2(pk2(0.05592203512787819f, 0.05592203512787819f), f,
+                       pk2(0.24264007806777954f, 0.24264007806777954f));
+    p = ffma2(p, f, pk2(0.6931210160255432f, 0.6931210160255432f));
+    p = ffma2(p, f, pk2(0.9999244809150696f, 0.9999244809150696f));
+    const uint32_t r0 = (uint32_t)p + ((uint32_t)t << 23);
+    const uint32_t r1 = (uint32_t)(p >> 32) + ((uint32_t)(t >> 32) << 23);
+    return (uint64_t)r0 | ((uint64_t)r1 << 32);
+}
+
+struct Params {
+    Tc4Args a;
+    int32_t q_tiles;      // query tiles per segment
+    int32_t nsplit;       // key splits per segment
+    int32_t n_kv_tiles;   // key tiles per split (the last split may own fewer)
+    int32_t total_tiles;  // key tiles of the whole segment
+    int64_t n_items;      // q_tiles * nsplit * U * nseg
+};
+
+struct Item {
+    int qtile, split, useg, u, seg, kv_tile0, n_kv;
+};
+__device__ __forceinline__ Item decode(const Params& p, int64_t it) {
+    Item r;
+    r.qtile = (int)(it % p.q_tiles);
+    const int64_t rest = it / p.q_tiles;
+    r.split = (int)(rest % p.nsplit);
+    r.useg = (int)(rest / p.nsplit);
+    r.u = r.useg / p.a.nseg;
+    r.seg = r.useg % p.a.nseg;
+    r.kv_tile0 = r.split * p.n_kv_tiles;
+    r.n_kv = min(p.n_kv_tiles, p.total_tiles - r.kv_tile0);
+    return r;
+}
+
+template <int NB>
+struct Smem {
+    static constexpr int S = NB == 1 ? 4 : 2;             // KV stages
+    static constexpr uint32_t q_off = 0;                  // 2 Q buffers
+    static constexpr uint32_t kv_off = 2 * kTileBytes;
+    static constexpr uint32_t bar_off = kv_off + S * NB * kTileBytes;
+    // q_full[2], q_empty[2], kv_full[S], kv_empty[S], s_full[2], p_full[2], pv_done,
+    // o_full[2], o_empty[2]
+    static constexpr uint32_t n_bars = 4 + 2 * S + 5 + 4;
+    static constexpr uint32_t slot_off = bar_off + n_bars * 8;
+    // float [4 slots][2 halves][128 rows]: slots 0/1 per-tile max (double-buffered), 2 row
+    // sum and 3 entropy dot of the epilogue
+    static constexpr uint32_t xch_off = slot_off + 16;
+    static constexpr uint32_t bytes = xch_off + 4 * 2 * 128 * 4;
+    static constexpr uint32_t alloc = bytes + 1024;
+};
+
+template <int NB, int NO>
+__global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant__ Params p) {
+    using SM = Smem<NB>;
+    constexpr int S = SM::S;
+    constexpr int NOB = NO == 1 ? 2 : 1;  // O buffers
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::bar_off);
+    uint64_t* q_full = bars;              // [2]
+    uint64_t* q_empty = bars + 2;         // [2]
+    uint64_t* kv_full = bars + 4;         // [S]
+    uint64_t* kv_empty = kv_full + S;     // [S]
+    uint64_t* s_full = kv_empty + S;      // [2]
+    uint64_t* p_full = s_full + 2;        // [2]
+    uint64_t* pv_done = p_full + 2;
+    uint64_t* o_full = pv_done + 1;       // [2]
+    uint64_t* o_empty = o_full + 2;       // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM::slot_off);
+
+    const Tc4Args& a = p.a;
+    const int warp = warp_id();
+
+    if (warp == 0 && elect_one()) {
+        tma_prefetch_desc(&a.tmQ);
+        tma_prefetch_desc(&a.tmK);
+        if (NB == 2) tma_prefetch_desc(&a.tmV);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&q_full[i], 1);
+            mbar_init(&q_empty[i], 256);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_full[i], 256);
+            mbar_init(&o_full[i], 1);
+            mbar_init(&o_empty[i], 256);
+        }
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&kv_full[s], 1);
+            mbar_init(&kv_empty[s], 1);
+        }
+        mbar_init(pv_done, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tS0 = tmem, tO0 = tmem + 256;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ TMA producer
+        if (elect_one()) {
+            int64_t g = 0;
+            int n = 0;
+            for (int64_t it = blockIdx.x; it < p.n_items; it += gridDim.x, ++n) {
+                const Item w = decode(p, it);
+                const int qbuf = n & 1;
+                if (n >= 2) mbar_wait_sleep(&q_empty[qbuf], ((n >> 1) - 1) & 1);
+                const int qb = w.u / a.qH, qh = w.u % a.qH;
+                const int kb = w.u / a.kH, kh = w.u % a.kH;
+                uint8_t* sq = smem + SM::q_off + qbuf * kTileBytes;
+                mbar_arrive_expect_tx(&q_full[qbuf], kTileBytes);
+                tma_load_5d(sq, &a.tmQ, &q_full[qbuf], 0, w.qtile * kTile, w.seg, qh, qb);
+                tma_load_5d(sq + kPanel, &a.tmQ, &q_full[qbuf], 64, w.qtile * kTile, w.seg, qh, qb);
+                for (int j = 0; j < w.n_kv; ++j, ++g) {
+                    const int st = (int)(g % S);
+                    if (g >= S) mbar_wait_sleep(&kv_empty[st], ((g / S) - 1) & 1);
+                    uint8_t* skv = smem + SM::kv_off + st * NB * kTileBytes;
+                    const int row = (w.kv_tile0 + j) * kTile;
+                    mbar_arrive_expect_tx(&kv_full[st], NB * kTileBytes);
+                    tma_load_5d(skv, &a.tmK, &kv_full[st], 0, row, w.seg, kh, kb);
+                    tma_load_5d(skv + kPanel, &a.tmK, &kv_full[st], 64, row, w.seg, kh, kb);
+                    if (NB == 2) {
+                        tma_load_5d(skv + kTileBytes, &a.tmV, &kv_full[st], 0, row, w.seg, kh, kb);
+                        tma_load_5d(skv + kTileBytes + kPanel, &a.tmV, &kv_full[st], 64, row, w.seg, kh, kb);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);            // S = Q K^T, both K-major
+        constexpr uint32_t idPV = idesc_bf16(128, NO == 2 ? 256 : 128, 0, 1);  // O += P [K|]V, MN-major
+        const uint32_t q_addr = smem_u32(smem + SM::q_off);
+        const uint32_t kv_addr = smem_u32(smem + SM::kv_off);
+        if (elect_one()) {
+            // the PV of tile g-1 is issued after S(g): remember what it needs
+            int64_t pg = -1;   // flattened index of the pending PV
+            int pst = 0, pob = 0, pn = 0;
+            bool pfirst = false, plast = false;
+            auto issue_pv = [&]() {
+                mbar_wait_sleep(&p_full[pg & 1], (pg >> 1) & 1);
+                if (pfirst && pn >= NOB) mbar_wait_sleep(&o_empty[pob], ((pn / NOB) - 1) & 1);
+                tc_fence_after();
+                const uint32_t tP = tS0 + (uint32_t)(pg & 1) * 128;
+                const uint32_t vaddr = kv_addr + pst * NB * kTileBytes + ((NB == 2 && NO == 1) ? kTileBytes : 0);
+                const uint32_t tO = tO0 + (uint32_t)pob * 128;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    umma_ts(tO, tP + kk * 8, sdesc_sw128(vaddr + kk * 2048, kPanel, 1024), idPV,
+                            (!pfirst || kk > 0) ? 1u : 0u);
+                umma_commit(&kv_empty[pst]);
+                umma_commit(pv_done);
+                if (plast) umma_commit(&o_full[pob]);
+            };
+            int64_t g = 0;
+            int n = 0;
+            for (int64_t it = blockIdx.x; it < p.n_items; it += gridDim.x, ++n) {
+                const Item w = decode(p, it);
+                const int qbuf = n & 1;
+                mbar_wait_sleep(&q_full[qbuf], (n >> 1) & 1);
+                const uint32_t qa = q_addr + qbuf * kTileBytes;
+                for (int j = 0; j < w.n_kv; ++j, ++g) {
+                    const int st = (int)(g % S);
+                    mbar_wait_sleep(&kv_full[st], (g / S) & 1);
+                    tc_fence_after();
+                    const uint32_t kaddr = kv_addr + st * NB * kTileBytes;
+                    const uint32_t tS = tS0 + (uint32_t)(g & 1) * 128;
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const uint32_t off = (kk >> 2) * kPanel + (kk & 3) * 32;
+                        umma_ss(tS, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(kaddr + off, 16, 1024), idS, kk > 0);
+                    }
+                    umma_commit(&s_full[g & 1]);
+                    if (pg >= 0) issue_pv();
+                    pg = g;
+                    pst = st;
+                    pob = n % NOB;
+                    pn = n;
+                    pfirst = j == 0;
+                    plast = j == w.n_kv - 1;
+                }
+            }
+            if (pg >= 0) issue_pv();
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------------------ softmax / epilogue
+        const int h = (warp - 4) >> 2;      // column half of the score row
+        const int row = (warp & 3) * 32 + lane_id();  // TMEM lane == query row in tile
+        const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+        float* xch = reinterpret_cast<float*>(smem + SM::xch_off);  // [slot][half][row]
+        int64_t g = 0;
+        int n = 0;
+        for (int64_t it = blockIdx.x; it < p.n_items; it += gridDim.x, ++n) {
+            const Item w = decode(p, it);
+            const int qbuf = n & 1, ob = n % NOB;
+            const uint32_t tO = tO0 + (uint32_t)ob * 128 + lane_base;
+            const uint8_t* qsm = smem + SM::q_off + qbuf * kTileBytes;
+            const int grow = w.qtile * kTile + row;  // row within the segment
+            const bool valid = grow < a.q_len;
+            float c = 1.f;
+            if (a.cR && valid) c = a.cR[((int64_t)w.u * a.nseg + w.seg) * a.q_len + grow];
+            if (a.clamp_enabled) {
+                c = (c < a.clamp_min) ? a.clamp_min : c;
+            } else if (!(c > 0.f)) {
+                if (valid && h == 0) atomicExch(a.status, kStatusClampDomain);
+                c = 1.f;
+            }
+            const float scale2 = a.qscale * kLog2e / c;
+            const int kv_end = (w.kv_tile0 + w.n_kv) * kTile;
+            const int last_valid = kTile - (kv_end > a.kv_len ? kv_end - a.kv_len : 0) - 64 * h;  // in my half
+
+            if (a.check_finite) {
+                mbar_wait_sleep(&q_full[qbuf], (n >> 1) & 1);
+                bool bad = false;
+                // each half checks one 64-column panel of the row
+                const uint4* q4 = reinterpret_cast<const uint4*>(qsm + h * kPanel + row * 128);
+#pragma unroll
+                for (int x = 0; x < 8; ++x) {
+                    const uint4 v = q4[x ^ (row & 7)];  // rotate chunks across lanes: no bank conflicts
+                    const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        bad |= ((wd[e] & 0x7F80u) == 0x7F80u) || ((wd[e] & 0x7F800000u) == 0x7F800000u);
+                }
+                if (bad && valid) atomicExch(a.status, kStatusNonFiniteQ);
+            }
+
+            float m_run = -INFINITY, l_run = 0.f;  // l_run: this half's partial row sum
+            const uint64_t scale2x2 = pk2(scale2, scale2);
+            for (int j = 0; j < w.n_kv; ++j, ++g) {
+                const uint32_t tS = tS0 + (uint32_t)(g & 1) * 128 + lane_base;
+                mbar_wait_sleep(&s_full[g & 1], (g >> 1) & 1);
+                tc_fence_after();
+                uint32_t sr[64];
+                VMB_TMEM_LD32(tS + 64 * h + 0, (sr + 0));
+                VMB_TMEM_LD32(tS + 64 * h + 32, (sr + 32));
+                tmem_ld_wait();
+                float* s = reinterpret_cast<float*>(sr);
+                if (j == w.n_kv - 1 && last_valid < 64) {
+                    asm volatile("");  // keep this a real (rarely taken) branch, not 64 selects
+#pragma unroll
+                    for (int x = 0; x < 64; ++x)
+                        if (x >= last_valid) s[x] = kMasked;
+                }
+                float a0 = s[0], a1 = s[1], a2 = s[2], a3 = s[3];
+#pragma unroll
+                for (int x = 4; x < 60; x += 8) {
+                    a0 = fmax3(a0, s[x + 0], s[x + 1]);
+                    a1 = fmax3(a1, s[x + 2], s[x + 3]);
+                    a2 = fmax3(a2, s[x + 4], s[x + 5]);
+                    a3 = fmax3(a3, s[x + 6], s[x + 7]);
+                }
+                a0 = fmax3(a0, s[60], s[61]);
+                a1 = fmax3(a1, s[62], s[63]);
+                // exchange the half-row maxima (double-buffered slot: one barrier per tile)
+                float* slot = xch + (g & 1) * 256;
+                slot[h * 128 + row] = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
+                named_bar_sync(1, 256);
+                const float m_cand = fmaxf(slot[row], slot[128 + row]) * scale2;
+                bool rescale = false;
+                float alpha = 1.f;
+                if (j == 0) {
+                    m_run = m_cand;
+                } else {
+                    // both halves see the same m_cand: identical decisions
+                    const bool need = m_cand > m_run + kRescaleThreshold;
+                    if (__any_sync(0xffffffffu, need)) {
+                        const float m_new = fmaxf(m_run, m_cand);
+                        alpha = ex2(m_run - m_new);
+                        l_run *= alpha;
+                        m_run = m_new;
+                        rescale = true;
+                    }
+                }
+                const uint64_t negm2 = pk2(-m_run, -m_run);
+                const uint64_t* s2 = reinterpret_cast<const uint64_t*>(sr);
+                uint64_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+#pragma unroll
+                for (int cc = 0; cc < 2; ++cc) {
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int x = 0; x < 16; ++x) {
+                        const uint64_t t2 = ffma2(s2[cc * 16 + x], scale2x2, negm2);
+                        uint64_t pp;
+                        if ((x % VMB_EMU_PERIOD) == VMB_EMU_PERIOD - 1) pp = ex2_emu2(t2);
+                        else pp = pk2(ex2(lo2(t2)), ex2(hi2(t2)));
+                        switch (x & 3) {
+                            case 0: acc0 = fadd2(acc0, pp); break;
+                            case 1: acc1 = fadd2(acc1, pp); break;
+                            case 2: acc2 = fadd2(acc2, pp); break;
+                            default: acc3 = fadd2(acc3, pp); break;
+                        }
+                        pk[x] = pack_bf16(lo2(pp), hi2(pp));
+                    }
+                    VMB_TMEM_ST16(tS + 32 * h + cc * 16, pk);
+                }
+                const uint64_t acc = fadd2(fadd2(acc0, acc1), fadd2(acc2, acc3));
+                l_run += lo2(acc) + hi2(acc);
+                if (rescale) {
+                    // O must hold every earlier P V product of this item before it is rescaled;
+                    // each half rescales its half of the O columns
+                    mbar_wait_sleep(pv_done, (uint32_t)((g - 1) & 1));
+                    tc_fence_after();
+#pragma unroll
+                    for (int cc = 0; cc < 2 * NO; ++cc) {
+                        uint32_t orr[32];
+                        const uint32_t ta = tO + h * 64 * NO + cc * 32;
+                        VMB_TMEM_LD32(ta, orr);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int x = 0; x < 32; ++x) orr[x] = __float_as_uint(__uint_as_float(orr[x]) * alpha);
+                        VMB_TMEM_ST32(ta, orr);
+                    }
+                }
+                tmem_st_wait();
+                tc_fence_before();
+                mbar_arrive(&p_full[g & 1]);
+            }
+
+            // -------------------------------------------------------- epilogue
+            // full row sum from the two halves
+            float* lx = xch + 2 * 256;
+            lx[h * 128 + row] = l_run;
+            named_bar_sync(1, 256);
+            const float l_tot = lx[row] + lx[128 + row];
+            mbar_wait_sleep(&o_full[ob], (n / NOB) & 1);
+            tc_fence_after();
+            const float inv_l = 1.f / l_tot;
+            const float lse2 = m_run + log2f(l_tot);  // base-2 log-sum-exp of x' = s * scale2
+            if (a.part_o) {
+                // split-KV partial: normalised fp32 O (this half's 64 columns) and the lse
+                float* prow = a.part_o + (((int64_t)w.useg * a.nsplit + w.split) * a.q_len + grow) * 128 + 64 * h;
+#pragma unroll
+                for (int cc = 0; cc < 2; ++cc) {
+                    uint32_t orr[32];
+                    VMB_TMEM_LD32(tO + 64 * h + cc * 32, orr);
+                    tmem_ld_wait();
+                    if (valid) {
+                        float4* dst = reinterpret_cast<float4*>(prow + cc * 32);
+#pragma unroll
+                        for (int x = 0; x < 8; ++x)
+                            dst[x] = make_float4(__uint_as_float(orr[4 * x + 0]) * inv_l, __uint_as_float(orr[4 * x + 1]) * inv_l,
+                                                 __uint_as_float(orr[4 * x + 2]) * inv_l, __uint_as_float(orr[4 * x + 3]) * inv_l);
+                    }
+                }
+                if (valid && h == 0) a.part_lse[((int64_t)w.useg * a.nsplit + w.split) * a.q_len + grow] = kLn2 * lse2;
+            } else {
+                float qo = 0.f;  // this half's part of <q_row, (P K)_row> (R-step entropy)
+                const int64_t obh = w.u / a.oHn, ohh = w.u % a.oHn;
+#pragma unroll
+                for (int t = 0; t < NO; ++t) {
+                    __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(t == 0 ? a.out0 : a.out1) + obh * a.oB[t] +
+                                          ohh * a.oH[t] + (int64_t)w.seg * a.oS[t] + (int64_t)grow * a.oR[t] + 64 * h;
+#pragma unroll
+                    for (int cc = 0; cc < 2; ++cc) {
+                        uint32_t orr[32];
+                        VMB_TMEM_LD32(tO + t * 128 + 64 * h + cc * 32, orr);
+                        tmem_ld_wait();
+                        if (t == 0 && a.cl_out) {
+                            const uint8_t* qp = qsm + h * kPanel;  // columns [64h, 64h+64)
+#pragma unroll
+                            for (int x = 0; x < 4; ++x) {
+                                const uint4 qv = *reinterpret_cast<const uint4*>(qp + sw128_offset(row, cc * 32 + 8 * x));
+                                const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    qo = fmaf(__uint_as_float(qw[e] << 16), __uint_as_float(orr[8 * x + 2 * e]), qo);
+                                    qo = fmaf(__uint_as_float(qw[e] & 0xFFFF0000u), __uint_as_float(orr[8 * x + 2 * e + 1]), qo);
+                                }
+                            }
+                        }
+                        if (valid) {
+                            uint4* dst = reinterpret_cast<uint4*>(orow + cc * 32);
+#pragma unroll
+                            for (int x = 0; x < 4; ++x) {
+                                uint4 v;
+                                v.x = pack_bf16(__uint_as_float(orr[8 * x + 0]) * inv_l, __uint_as_float(orr[8 * x + 1]) * inv_l);
+                                v.y = pack_bf16(__uint_as_float(orr[8 * x + 2]) * inv_l, __uint_as_float(orr[8 * x + 3]) * inv_l);
+                                v.z = pack_bf16(__uint_as_float(orr[8 * x + 4]) * inv_l, __uint_as_float(orr[8 * x + 5]) * inv_l);
+                                v.w = pack_bf16(__uint_as_float(orr[8 * x + 6]) * inv_l, __uint_as_float(orr[8 * x + 7]) * inv_l);
+                                dst[x] = v;
+                            }
+                        }
+                    }
+                }
+                if (a.cl_out) {
+                    // combine the two halves of the entropy dot product
+                    float* qx = xch + 3 * 256;
+                    qx[h * 128 + row] = qo;
+                    named_bar_sync(1, 256);
+                    qo = qx[row] + qx[128 + row];
+                }
+                if (valid && h == 0) {
+                    if (a.cl_out)
+                        a.cl_out[((int64_t)w.u * a.q_len + grow) * a.nseg + w.seg] = kLn2 * (scale2 * qo * inv_l - lse2);
+                    if (a.lse_out) a.lse_out[((int64_t)w.u * a.nseg + w.seg) * a.q_len + grow] = kLn2 * lse2;
+                }
+            }
+            // O buffer and Q buffer of this item are free for the items two ahead
+            tc_fence_before();
+            mbar_arrive(&o_empty[ob]);
+            mbar_arrive(&q_empty[qbuf]);
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
+template <int NB, int NO>
+void launch(const Params& p, cudaStream_t s) {
+    using SM = Smem<NB>;
+    auto kern = fa4_kernel<NB, NO>;
+    VMB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM::alloc));
+    int dev = 0, sms = 148;
+    VMB_CHECK_CUDA(cudaGetDevice(&dev));
+    VMB_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int64_t grid = std::min<int64_t>(p.n_items, sms);
+    ProfScope ps(NO == 2 ? kKRstepY : (NB == 1 ? kKRstep : kKAttn), s);
+    kern<<<(unsigned)grid, kThreads, SM::alloc, s>>>(p);
+    count_launch();
+    check_launch("fa4_tc");
+}
+
+}  // namespace
+
+int tc4_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg, int max_split) {
+    if (max_split <= 1 || q_len <= 0 || n_useg <= 0) return 1;
+    const int64_t total_tiles = (kv_len + kTile - 1) / kTile;
+    // ~16 items per SM so the persistent CTAs balance, >= 8 key tiles per split
+    const int64_t base = ((q_len + kTile - 1) / kTile) * n_useg;
+    const int64_t want = (16 * 148 + base - 1) / base;
+    int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>({want, (int64_t)max_split, total_tiles / 8}));
+    while (nsplit > 1 && ((total_tiles + nsplit - 1) / nsplit) * (nsplit - 1) >= total_tiles) --nsplit;
+    return nsplit;
+}
+
+void tc4_fa_launch(Tc4Args a, int64_t U, cudaStream_t s) {
+    if (U == 0 || a.q_len == 0) return;
+    VMB_REQUIRE_DIM(a.kv_len >= 1, "attention over empty keys");
+    VMB_REQUIRE_DIM(a.nv == 1 || a.nv == 2, "value operand count");
+    VMB_REQUIRE_DIM(!a.cl_out || a.v_is_k || a.nv == 2, "entropy output needs the key tile as first value operand");
+    Params p;
+    p.q_tiles = (a.q_len + kTile - 1) / kTile;
+    p.total_tiles = (a.kv_len + kTile - 1) / kTile;
+    const int64_t n_useg = U * a.nseg;
+    p.nsplit = (a.part_o && a.nv == 1 && !a.v_is_k) ? tc4_plan_splits(a.q_len, a.kv_len, n_useg, a.max_split) : 1;
+    p.n_kv_tiles = (p.total_tiles + p.nsplit - 1) / p.nsplit;
+    p.n_items = (int64_t)p.q_tiles * p.nsplit * n_useg;
+    a.nsplit = p.nsplit;
+    if (p.nsplit == 1) a.part_o = nullptr;
+    p.a = a;
+    if (a.nv == 2) launch<2, 2>(p, s);
+    else if (a.v_is_k) launch<1, 1>(p, s);
+    else launch<2, 1>(p, s);
+    if (p.nsplit > 1) {
+        Tc2Args c{};
+        c.q_len = a.q_len;
+        c.nseg = a.nseg;
+        c.oHn = a.oHn;
+        c.out = a.out0;
+        c.oB = a.oB[0]; c.oH = a.oH[0]; c.oS = a.oS[0]; c.oR = a.oR[0];
+        c.lse_out = a.lse_out;
+        c.part_o = a.part_o;
+        c.part_lse = a.part_lse;
+        c.nsplit = p.nsplit;
+        c.n_useg = n_useg;
+        tc2_combine_launch(c, s);
+    }
+}
+
+}  // namespace vmb

@@ -46,17 +46,33 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
     asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
     return d;
 }
-// 2^x on the FMA/ALU pipes: n = rint(x) via the 1.5*2^23 magic, 2^(x-n) by a degree-3
-// minimax polynomial on [-0.5, 0.5] (rel. err 1.1e-4, far below bf16 P rounding), then n is
-// added to the exponent field.  x is clamped at -126 (2^-126 is 0 for every purpose here).
-__device__ __forceinline__ float ex2_emu(float x) {
-    x = fmaxf(x, -126.f);
-    const float kMagic = 12582912.f;
-    const float t = x + kMagic;
-    const float f = x - (t - kMagic);
-    const float p = fmaf(fmaf(fmaf(0.05592203512787819f, f, 0.24264007806777954f), f, 0.6931210160255432f), f,
-                         0.9999244809150696f);
-    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+__device__ __forceinline__ uint64_t ffma2(uint64_t x, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(x), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t x, uint64_t y) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(x), "l"(y));
+    return d;
+}
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+    return (uint64_t)__float_as_uint(lo) | ((uint64_t)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ float lo2(uint64_t v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float hi2(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+// 2^x for an element pair on the FMA/ALU pipes (see fa3_tc.cu)
+__device__ __forceinline__ uint64_t ex2_emu2(uint64_t x2) {
+    const uint64_t xx = pk2(fmaxf(lo2(x2), -126.f), fmaxf(hi2(x2), -126.f));
+    const uint64_t t = fadd2(xx, pk2(12582912.f, 12582912.f));
+    const uint64_t f = fadd2(xx, fadd2(pk2(-12582912.f, -12582912.f), t) ^ 0x8000000080000000ull);
+    uint64_t p = ffma2(pk2(0.05592203512787819f, 0.05592203512787819f), f,
+                       pk2(0.24264007806777954f, 0.24264007806777954f));
+    p = ffma2(p, f, pk2(0.6931210160255432f, 0.6931210160255432f));
+    p = ffma2(p, f, pk2(0.9999244809150696f, 0.9999244809150696f));
+    const uint32_t r0 = (uint32_t)p + ((uint32_t)t << 23);
+    const uint32_t r1 = (uint32_t)(p >> 32) + ((uint32_t)(t >> 32) << 23);
+    return (uint64_t)r0 | ((uint64_t)r1 << 32);
 }
 
 template <int NB>
@@ -141,7 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
             tma_load_5d(sq + kPanelBytes, &a.tmQ, q_full, 64, qtile * kTile, seg, qh, qb);
             for (int j = 0; j < n_kv; ++j) {
                 const int st = j % S;
-                if (j >= S) mbar_wait(&kv_empty[st], ((j / S) + 1) & 1);
+                if (j >= S) mbar_wait_sleep(&kv_empty[st], ((j / S) + 1) & 1);
                 uint8_t* skv = smem + SM::kv_off + st * NB * kTileBytes;
                 mbar_arrive_expect_tx(&kv_full[st], NB * kTileBytes);
                 tma_load_5d(skv, &a.tmK, &kv_full[st], 0, j * kTile, kseg, kh, kb);
@@ -157,14 +173,15 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
         // ------------------------------------------------------------ MMA issuer
         constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);   // S = Q K^T, both K-major
         constexpr uint32_t idPV = idesc_bf16(128, 128, 0, 1);  // O += P V, V MN-major
+        constexpr uint32_t idPV2 = idesc_bf16(128, 256, 0, 1); // O += P [K | V]
         const uint32_t q_addr = smem_u32(smem + SM::q_off);
         const uint32_t kv_addr = smem_u32(smem + SM::kv_off);
         if (elect_one()) {
-            mbar_wait(q_full, 0);
+            mbar_wait_sleep(q_full, 0);
             for (int j = 0; j <= n_kv; ++j) {
                 if (j < n_kv) {
                     const int st = j % S;
-                    mbar_wait(&kv_full[st], (j / S) & 1);
+                    mbar_wait_sleep(&kv_full[st], (j / S) & 1);
                     tc_fence_after();
                     const uint32_t kaddr = kv_addr + st * NB * kTileBytes;
                     const uint32_t tS = tS0 + (j & 1) * 128;
@@ -178,20 +195,24 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
                 }
                 if (j >= 1) {
                     const int jp = j - 1, st = jp % S;
-                    mbar_wait(&p_full[jp & 1], (jp >> 1) & 1);
+                    mbar_wait_sleep(&p_full[jp & 1], (jp >> 1) & 1);
                     tc_fence_after();
                     const uint32_t tP = tS0 + (jp & 1) * 128;
                     const uint32_t kaddr = kv_addr + st * NB * kTileBytes;
+                    if (NO == 2) {
+                        // O[:, 0:256) += P [K | V]: one N = 256 MMA per k-step (the K and V
+                        // tiles are adjacent 2-panel tiles, so the four 64-column panels of the
+                        // B operand are uniformly strided); N = 256 is the full-rate shape
 #pragma unroll
-                    for (int t = 0; t < NO; ++t) {
-                        // value operand: K tile (NB == 1, or t == 0 of [K|V]) else V tile
-                        const uint32_t vaddr = kaddr + ((NB == 2 && (NO == 1 || t == 1)) ? kTileBytes : 0);
-#pragma unroll
-                        for (int kk = 0; kk < 8; ++kk) {
-                            umma_ts(tO + t * 128, tP + kk * 8,
-                                    sdesc_sw128(vaddr + kk * 2048, kPanelBytes, 1024), idPV,
+                        for (int kk = 0; kk < 8; ++kk)
+                            umma_ts(tO, tP + kk * 8, sdesc_sw128(kaddr + kk * 2048, kPanelBytes, 1024), idPV2,
                                     (jp > 0 || kk > 0) ? 1u : 0u);
-                        }
+                    } else {
+                        const uint32_t vaddr = kaddr + (NB == 2 ? kTileBytes : 0);
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk)
+                            umma_ts(tO, tP + kk * 8, sdesc_sw128(vaddr + kk * 2048, kPanelBytes, 1024), idPV,
+                                    (jp > 0 || kk > 0) ? 1u : 0u);
                     }
                     umma_commit(&kv_empty[st]);
                     umma_commit(pv_done);
@@ -217,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
         const int last_valid = a.kv_len - (n_kv - 1) * kTile;  // valid keys in the last tile
 
         if (a.check_finite) {
-            mbar_wait(q_full, 0);
+            mbar_wait_sleep(q_full, 0);
             const uint4* q0 = reinterpret_cast<const uint4*>(smem + SM::q_off + row * 128);
             const uint4* q1 = reinterpret_cast<const uint4*>(smem + SM::q_off + kPanelBytes + row * 128);
             bool bad = false;
@@ -233,10 +254,17 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
         }
 
         float m_run = -INFINITY, l_run = 0.f;
+        const uint64_t scale2x2 = pk2(scale2, scale2);
         for (int j = 0; j < n_kv; ++j) {
             const uint32_t tS = tS0 + (j & 1) * 128 + lane_base;
-            mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+            mbar_wait_sleep(&s_full[j & 1], (j >> 1) & 1);
             tc_fence_after();
+#if VMB_DEBUG_NO_SOFTMAX  // timing experiment only: MMA/TMA pipeline without the softmax
+            if (true) {
+                mbar_arrive(&p_full[j & 1]);
+                continue;
+            }
+#endif
             uint32_t sr[128];
             VMB_TMEM_LD32(tS + 0, (sr + 0));
             VMB_TMEM_LD32(tS + 32, (sr + 32));
@@ -245,6 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
             tmem_ld_wait();
             float* s = reinterpret_cast<float*>(sr);
             if (j == n_kv - 1 && last_valid < kTile) {
+                asm volatile("");  // keep this a real (rarely taken) branch, not 128 selects
 #pragma unroll
                 for (int x = 0; x < 128; ++x)
                     if (x >= last_valid) s[x] = kMasked;
@@ -261,61 +290,73 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
             a0 = fmax3(a0, s[124], s[125]);
             a1 = fmax3(a1, s[126], s[127]);
             const float m_cand = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3)) * scale2;
+            bool rescale = false;
+            float alpha = 1.f;
             if (j == 0) {
                 m_run = m_cand;
             } else {
                 const bool need = m_cand > m_run + kRescaleThreshold;
                 if (__any_sync(0xffffffffu, need)) {
                     const float m_new = fmaxf(m_run, m_cand);
-                    const float alpha = ex2(m_run - m_new);
+                    alpha = ex2(m_run - m_new);
                     l_run *= alpha;
                     m_run = m_new;
-                    // O must hold every earlier P V product before it is rescaled
-                    mbar_wait(pv_done, (j - 1) & 1);
-                    tc_fence_after();
-#pragma unroll
-                    for (int t = 0; t < NO; ++t) {
-#pragma unroll
-                        for (int cc = 0; cc < 4; ++cc) {
-                            uint32_t orr[32];
-                            const uint32_t ta = tO + t * 128 + cc * 32 + lane_base;
-                            VMB_TMEM_LD32(ta, orr);
-                            tmem_ld_wait();
-#pragma unroll
-                            for (int x = 0; x < 32; ++x)
-                                orr[x] = __float_as_uint(__uint_as_float(orr[x]) * alpha);
-                            VMB_TMEM_ST32(ta, orr);
-                        }
-                    }
+                    rescale = true;
                 }
             }
-            const float neg_m = -m_run;
-            float l0 = 0.f, l1 = 0.f, l2 = 0.f, l3 = 0.f;
+            // x' - m on the packed FMA pipe; 2^(x' - m) on MUFU for 7 of 8 pairs and the FMA-pipe
+            // polynomial for the 8th (MUFU, 16 ex2/clk/SM, binds the softmax: SURVEY §7 hard
+            // part 4); packed row sums; P -> TMEM as bf16
+            const uint64_t negm2 = pk2(-m_run, -m_run);
+            const uint64_t* s2 = reinterpret_cast<const uint64_t*>(sr);
+            uint64_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
 #pragma unroll
             for (int cc = 0; cc < 4; ++cc) {
                 uint32_t pk[16];
 #pragma unroll
                 for (int x = 0; x < 16; ++x) {
-                    const float t0 = fmaf(s[cc * 32 + 2 * x], scale2, neg_m);
-                    const float t1 = fmaf(s[cc * 32 + 2 * x + 1], scale2, neg_m);
-                    // one pair in four goes through the FMA pipe: the MUFU pipe (16 ex2/clk/SM)
-                    // is the softmax's binding unit (SURVEY §7 hard part 4)
-                    const bool emu = (x & 3) == 3;
-                    const float p0 = emu ? ex2_emu(t0) : ex2(t0);
-                    const float p1 = emu ? ex2_emu(t1) : ex2(t1);
-                    if ((x & 1) == 0) { l0 += p0; l1 += p1; } else { l2 += p0; l3 += p1; }
-                    pk[x] = pack_bf16(p0, p1);
+                    const uint64_t t2 = ffma2(s2[cc * 16 + x], scale2x2, negm2);
+                    uint64_t pp;
+                    if ((x % VMB_EMU_PERIOD) == VMB_EMU_PERIOD - 1) pp = ex2_emu2(t2);
+                    else pp = pk2(ex2(lo2(t2)), ex2(hi2(t2)));
+                    switch (x & 3) {
+                        case 0: acc0 = fadd2(acc0, pp); break;
+                        case 1: acc1 = fadd2(acc1, pp); break;
+                        case 2: acc2 = fadd2(acc2, pp); break;
+                        default: acc3 = fadd2(acc3, pp); break;
+                    }
+                    pk[x] = pack_bf16(lo2(pp), hi2(pp));
                 }
                 VMB_TMEM_ST16(tS + cc * 16, pk);
             }
-            l_run += (l0 + l1) + (l2 + l3);
+            const uint64_t acc = fadd2(fadd2(acc0, acc1), fadd2(acc2, acc3));
+            l_run += lo2(acc) + hi2(acc);
+            if (rescale) {
+                // O must hold every earlier P V product before it is rescaled; P_j V is not
+                // issued before this thread arrives on p_full
+                mbar_wait_sleep(pv_done, (j - 1) & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int t = 0; t < NO; ++t) {
+#pragma unroll
+                    for (int cc = 0; cc < 4; ++cc) {
+                        uint32_t orr[32];
+                        const uint32_t ta = tO + t * 128 + cc * 32 + lane_base;
+                        VMB_TMEM_LD32(ta, orr);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int x = 0; x < 32; ++x) orr[x] = __float_as_uint(__uint_as_float(orr[x]) * alpha);
+                        VMB_TMEM_ST32(ta, orr);
+                    }
+                }
+            }
             tmem_st_wait();
             tc_fence_before();
             mbar_arrive(&p_full[j & 1]);
         }
 
         // ------------------------------------------------------------ epilogue
-        mbar_wait(o_full, 0);
+        mbar_wait_sleep(o_full, 0);
         tc_fence_after();
         const float inv_l = 1.f / l_run;
         const int64_t ob = u / a.oHn, oh = u % a.oHn;
@@ -403,7 +444,7 @@ void tc_fa_launch(const TcFaArgs& a, int64_t U, cudaStream_t s) {
     p.n_kv_tiles = (a.kv_len + kTile - 1) / kTile;
     if (a.nv == 2) launch<2, 2>(p, U, s);
     else if (a.v_is_k) launch<1, 1>(p, U, s);
-    else launch<2, 1>(p, U, s);
+    else VMB_REQUIRE_DIM(false, "fa_tc serves the R half-steps only");
 }
 
 }  // namespace vmb

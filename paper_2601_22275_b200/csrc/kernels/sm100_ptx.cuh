@@ -77,9 +77,24 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t pari
         : "memory");
     return ok != 0;
 }
+// One exponential pair in VMB_EMU_PERIOD goes through the FMA-pipe polynomial instead of
+// MUFU (0 < period; a period larger than the pair count disables the emulation).  Measured
+// on B200 (profiles/r1_fa_variants.md): MUFU is not the binding unit of these kernels, so
+// the emulation is off by default.
+#ifndef VMB_EMU_PERIOD
+#define VMB_EMU_PERIOD 64
+#endif
+#ifndef VMB_SLEEP_WAIT
+#define VMB_SLEEP_WAIT 0
+#endif
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+#if VMB_SLEEP_WAIT
     while (!mbar_try_wait_sleep(bar, parity)) {
     }
+#else
+    while (!mbar_try_wait(bar, parity)) {
+    }
+#endif
 }
 
 // ---------------------------------------------------------------- TMA

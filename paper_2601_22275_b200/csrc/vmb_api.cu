@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -117,10 +118,89 @@ CUtensorMap make_tmap_bf16_5d(const void* base, const uint64_t dims[5], const ui
     return map;
 }
 
+int attn_impl(bool rstep) {
+    // Kernel family per call site (A/B switches for measurements):
+    //   R half-steps (VMB_RSTEP): 2 = fa2 (default: 2 CTAs/SM, 64-key tiles) with fa_tc for
+    //     the last (y-fused) step, 1 = fa_tc for both, 4 = fa4 persistent for both
+    //     (profiles/r1_fa_variants.md has the measurements behind the default)
+    //   attention over all N keys: recompute / flash / dense (VMB_ATTN): 3 = fa3 (default),
+    //     4 = fa4 persistent, 2 = fa2
+    static const int r = [] {
+        const char* e = getenv("VMB_RSTEP");
+        const int v = e ? atoi(e) : 2;
+        return (v == 1 || v == 4) ? v : 2;
+    }();
+    static const int at = [] {
+        const char* e = getenv("VMB_ATTN");
+        const int v = e ? atoi(e) : 3;
+        return (v == 2 || v == 4) ? v : 3;
+    }();
+    return rstep ? r : at;
+}
+
 namespace {
 
 constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
+// key-tile rows of the attention kernel family in use (the K/V TMA box height)
+uint32_t attn_kv_box(bool rstep) { return attn_impl(rstep) == 2 ? (uint32_t)tc2_kv_tile(1) : 128u; }
+int attn_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg) {
+    switch (attn_impl(false)) {
+        case 2: return tc2_plan_splits(q_len, kv_len, n_useg, 2, kTc2MaxSplit);
+        case 4: return tc4_plan_splits(q_len, kv_len, n_useg, kTc2MaxSplit);
+        default: return tc3_plan_splits(q_len, kv_len, n_useg, kTc2MaxSplit);
+    }
+}
+Tc4Args to_tc4(const Tc2Args& a) {
+    Tc4Args r{};
+    r.tmQ = a.tmQ; r.tmK = a.tmK; r.tmV = a.tmV;
+    r.nseg = a.nseg; r.q_len = a.q_len; r.kv_len = a.kv_len;
+    r.qH = a.qH; r.kH = a.kH; r.oHn = a.oHn;
+    r.cR = a.cR; r.qscale = a.qscale; r.clamp_min = a.clamp_min; r.clamp_enabled = a.clamp_enabled;
+    r.nv = 1;
+    r.v_is_k = a.nv == 1;
+    r.out0 = a.out;
+    r.oB[0] = a.oB; r.oH[0] = a.oH; r.oS[0] = a.oS; r.oR[0] = a.oR;
+    r.cl_out = a.cl_out; r.lse_out = a.lse_out; r.status = a.status; r.check_finite = a.check_finite;
+    r.part_o = a.part_o; r.part_lse = a.part_lse; r.max_split = a.max_split;
+    return r;
+}
+Tc4Args to_tc4(const TcFaArgs& a) {
+    Tc4Args r{};
+    r.tmQ = a.tmQ; r.tmK = a.tmK; r.tmV = a.tmV;
+    r.nseg = a.nseg; r.q_len = a.q_len; r.kv_len = a.kv_len;
+    r.qH = a.qH; r.kH = a.kH; r.oHn = a.oHn;
+    r.cR = a.cR; r.qscale = a.qscale; r.clamp_min = a.clamp_min; r.clamp_enabled = a.clamp_enabled;
+    r.nv = a.nv; r.v_is_k = a.v_is_k;
+    r.out0 = a.out0; r.out1 = a.out1;
+    for (int t = 0; t < 2; ++t) { r.oB[t] = a.oB[t]; r.oH[t] = a.oH[t]; r.oS[t] = a.oS[t]; r.oR[t] = a.oR[t]; }
+    r.cl_out = a.cl_out; r.lse_out = a.lse_out; r.status = a.status; r.check_finite = a.check_finite;
+    r.max_split = 1;
+    return r;
+}
+// a.nv == 2: value operand V (attention); a.nv == 1: value = key (R half-step)
+void attn_launch(const Tc2Args& a, int64_t U, cudaStream_t s, bool rstep) {
+    switch (attn_impl(rstep)) {
+        case 2: tc2_fa_launch(a, U, s); break;
+        case 4: tc4_fa_launch(to_tc4(a), U, s); break;
+        case 1:  // original 1-CTA/SM kernel (R half-step only)
+        default:
+            if (rstep && attn_impl(true) == 1) {
+                TcFaArgs f{};
+                f.tmQ = a.tmQ; f.tmK = a.tmK; f.tmV = a.tmV;
+                f.nseg = a.nseg; f.q_len = a.q_len; f.kv_len = a.kv_len;
+                f.qH = a.qH; f.kH = a.kH; f.oHn = a.oHn;
+                f.cR = a.cR; f.qscale = a.qscale; f.clamp_min = a.clamp_min; f.clamp_enabled = a.clamp_enabled;
+                f.nv = 1; f.v_is_k = 1;
+                f.out0 = a.out; f.oB[0] = a.oB; f.oH[0] = a.oH; f.oS[0] = a.oS; f.oR[0] = a.oR;
+                f.cl_out = a.cl_out; f.lse_out = a.lse_out; f.status = a.status; f.check_finite = a.check_finite;
+                tc_fa_launch(f, U, s);
+            } else {
+                tc3_fa_launch(a, U, s);
+            }
+            break;
+    }
+}
 
 struct Shape {
     int64_t T, h, w, d, H, B, U, N, m, b, hw;
@@ -185,7 +265,7 @@ Workspace carve(void* base, const Shape& s, vmb_dtype dt) {
     w.part_o = w.part_lse = nullptr;
     w.nsplit = 1;
     if (dt == VMB_BF16 && s.d == 128 && s.recompute && s.U > 0) {
-        w.nsplit = tc2_plan_splits(s.hw, s.N, s.U, 2, kTc2MaxSplit);
+        w.nsplit = attn_plan_splits(s.hw, s.N, s.U);
         if (w.nsplit > 1) {
             w.part_o = reinterpret_cast<float*>(p + off);
             off += align_up((size_t)s.U * w.nsplit * s.hw * 128 * sizeof(float));
@@ -303,7 +383,7 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
         const CUtensorMap mQrow = user_map(q, in, s, b, 1, m, b, 128, 1);    // (d, i, k): query tiles
         const CUtensorMap mK = user_map(k, in, s, b, 1, m, b, 128, 1);
         const CUtensorMap mV = user_map(v, in, s, b, 1, m, b, 128, 1);
-        const CUtensorMap mK2 = user_map(k, in, s, b, 1, m, b, (uint32_t)tc2_kv_tile(1), 1);  // fa2 key tiles
+        const CUtensorMap mK2 = user_map(k, in, s, b, 1, m, b, attn_kv_box(true), 1);  // attention key tiles
         const uint32_t lrows = (uint32_t)lstep_rows(m);
         const CUtensorMap mQcol = user_map(q, in, s, b, 1, m, b, 1, lrows);   // (d, i, j): Qb[i] boxes
         const CUtensorMap mAR = internal_map(ws.aR, U, m, b, d, true, 128, 1);  // aR (U,m,b,d): (d,i,k) query tiles
@@ -338,7 +418,9 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
             fa.status = ws.status;
             fa.check_finite = t == 0;
             if (last) {
-                tc_fa_launch(fa, U, st);
+                // last R half-step with y = R V fused: O = P [K | V]
+                if (attn_impl(true) == 4) tc4_fa_launch(to_tc4(fa), U, st);
+                else tc_fa_launch(fa, U, st);
             } else {
                 // R half-step without y: the 2-CTA/SM kernel (value operand = key tile)
                 Tc2Args f2{};
@@ -362,7 +444,7 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
                 f2.status = ws.status;
                 f2.check_finite = fa.check_finite;
                 f2.max_split = 1;
-                tc2_fa_launch(f2, U, st);
+                attn_launch(f2, U, st, true);
             }
 
             TcLstepArgs ls{};
@@ -384,7 +466,7 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
         if (recompute) {
             // first-frame recompute: Q[0:hw) against all N keys, split over the keys
             const int64_t Hm = std::max<int64_t>(s.H, 1);
-            const uint32_t bn = (uint32_t)tc2_kv_tile(2);
+            const uint32_t bn = attn_kv_box(false);
             Tc2Args f2{};
             f2.tmQ = user_map(q, in, s, s.hw, 1, 1, s.hw, 128, 1);
             f2.tmK = user_map(k, in, s, s.N, 1, 1, s.N, bn, 1);
@@ -401,7 +483,7 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
             f2.part_o = ws.part_o;
             f2.part_lse = ws.part_lse;
             f2.max_split = ws.part_o ? kTc2MaxSplit : 1;
-            tc2_fa_launch(f2, U, st);
+            attn_launch(f2, U, st, false);
         }
         return;
     }
@@ -669,7 +751,7 @@ vmb_status vmb_rstep(int64_t units, int64_t m, int64_t b, int64_t d, vmb_dtype d
         if (tc) {
             Tc2Args f2{};
             f2.tmQ = internal_map(aR, units, m, b, d, true, 128, 1);
-            f2.tmK = internal_map(Kb, units, m, b, d, true, (uint32_t)tc2_kv_tile(1), 1);
+            f2.tmK = internal_map(Kb, units, m, b, d, true, attn_kv_box(true), 1);
             f2.tmV = f2.tmK;
             f2.nseg = (int32_t)m;
             f2.q_len = f2.kv_len = (int32_t)b;
@@ -686,7 +768,7 @@ vmb_status vmb_rstep(int64_t units, int64_t m, int64_t b, int64_t d, vmb_dtype d
             int32_t* dummy = nullptr;
             VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dummy), sizeof(int32_t), st));
             f2.status = dummy;
-            tc2_fa_launch(f2, units, st);
+            attn_launch(f2, units, st, true);
             VMB_CHECK_CUDA(cudaFreeAsync(dummy, st));
             return;
         }
@@ -771,7 +853,7 @@ vmb_status vmb_flash_entropy_fwd(int64_t units, int64_t nq, int64_t nk, int64_t 
                         aligned16(v) && aligned16(o) && nq <= INT32_MAX && nk <= INT32_MAX;
         if (tc) {
             Tc2Args f2{};
-            const uint32_t bn = (uint32_t)tc2_kv_tile(2);
+            const uint32_t bn = attn_kv_box(false);
             const uint64_t sq = (uint64_t)(nq * d * 2), sk = (uint64_t)(nk * d * 2);
             const uint64_t dq[5] = {(uint64_t)d, (uint64_t)nq, 1, 1, (uint64_t)std::max<int64_t>(units, 1)};
             const uint64_t dk[5] = {(uint64_t)d, (uint64_t)nk, 1, 1, (uint64_t)std::max<int64_t>(units, 1)};
@@ -791,7 +873,7 @@ vmb_status vmb_flash_entropy_fwd(int64_t units, int64_t nq, int64_t nk, int64_t 
             f2.out = o;
             f2.oB = nq * d; f2.oH = 0; f2.oS = 0; f2.oR = d;
             f2.lse_out = lse;
-            const int nsplit = tc2_plan_splits(nq, nk, units, 2, kTc2MaxSplit);
+            const int nsplit = attn_plan_splits(nq, nk, units);
             float* part = nullptr;
             int32_t* dummy = nullptr;
             VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dummy), sizeof(int32_t), st));
@@ -805,7 +887,7 @@ vmb_status vmb_flash_entropy_fwd(int64_t units, int64_t nq, int64_t nk, int64_t 
                 f2.max_split = 1;
             }
             f2.status = dummy;
-            tc2_fa_launch(f2, units, st);
+            attn_launch(f2, units, st, false);
             if (part) VMB_CHECK_CUDA(cudaFreeAsync(part, st));
             VMB_CHECK_CUDA(cudaFreeAsync(dummy, st));
             return;
