@@ -37,6 +37,7 @@ CONFIGS = {
     "c4": (81, 28, 52, 40, 128, "C4: 321-frame 448x832 latent 81x28x52 (N=117936), H=40, d=128, bf16, t=2"),
     "c3": (21, 30, 52, 40, 128, "C3: Wan-2.1-14B 21x30x52 latent (N=32760), H=40, d=128, bf16, t=2"),
     "c2": (21, 30, 52, 12, 128, "C2: Wan-2.1-1.3B 21x30x52 latent (N=32760), H=12, d=128, bf16, t=2"),
+    "c5": (81, 112, 104, 40, 128, "C5: long-video stress 81x112x104 latent (N=943488), H=40, d=128, bf16, t=2"),
 }
 KERNEL_NAMES = ["rstep", "rstep_y", "attn_recompute", "lstep", "lstep_apply", "simt", "combine"]
 
@@ -109,15 +110,17 @@ def flops_per_call(grid, vm):
     return (rep.monarch_flops + rep.recompute_flops) * grid.units(), rep
 
 
-def kernel_algorithmic(grid, units):
-    """Algorithmic work per launch: FLOPs for tensor-bound, bytes for HBM-bound."""
+def kernel_algorithmic(grid, units, qfrac=1.0):
+    """Algorithmic work per launch: FLOPs for tensor-bound, bytes for HBM-bound.
+    qfrac: fraction of the query rows this rank owns (sequence-sharded mode)."""
     N, d, m, b, hw = grid.tokens(), grid.head_dim, grid.t_frames, grid.h * grid.w, grid.h * grid.w
+    Nq = N * qfrac
     return {
-        "rstep": ("tensor", units * 4.0 * N * b * d),            # S = aR K^T, aL = P K
-        "rstep_y": ("tensor", units * 6.0 * N * b * d),          # + y = P V
-        "attn_recompute": ("tensor", units * 4.0 * hw * N * d),  # Q0 K^T, P V
-        "lstep": ("hbm", units * (3 * 2.0 * N * d + 2 * 4.0 * N)),        # Qb, aL in; aR out; cL in, cR out
-        "lstep_apply": ("hbm", units * (4 * 2.0 * N * d + 4.0 * N)),     # Qb, aL, y in; O out; cL in
+        "rstep": ("tensor", units * 4.0 * Nq * b * d),            # S = aR K^T, aL = P K
+        "rstep_y": ("tensor", units * 6.0 * Nq * b * d),          # + y = P V
+        "attn_recompute": ("tensor", units * 4.0 * hw * qfrac * N * d),  # Q0 K^T, P V
+        "lstep": ("hbm", units * (3 * 2.0 * Nq * d + 2 * 4.0 * Nq)),     # Qb, aL in; aR out; cL in, cR out
+        "lstep_apply": ("hbm", units * (4 * 2.0 * Nq * d + 4.0 * Nq)),   # Qb, aL, y in; O out; cL in
     }
 
 
@@ -189,6 +192,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--shard", default="heads", choices=["heads", "seq"],
+                    help="multi-GPU split: heads (no inter-GPU traffic) or seq (spatial slabs, NCCL K/V all-gather)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -209,19 +214,45 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     T, h, w, heads, d, desc = CONFIGS[args.config]
-    # head sharding: contiguous blocks of heads per rank, no inter-GPU traffic
-    from paper_2601_22275_b200.dist import unit_shards
-    per = [b_ - a_ for a_, b_ in unit_shards(heads, world)]
-    my_heads = per[rank]
-    grid = vm.TokenGrid(T, h, w, d, my_heads, 1)
+    from paper_2601_22275_b200.dist import slab_partition, unit_shards
     cfg = vm.VMonarchConfig()
-    n = grid.tokens()
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
-    q = torch.randn((my_heads, n, d), device=dev, dtype=torch.bfloat16, generator=gen)
-    k = torch.randn((my_heads, n, d), device=dev, dtype=torch.bfloat16, generator=gen)
-    v = torch.randn((my_heads, n, d), device=dev, dtype=torch.bfloat16, generator=gen)
-    o = torch.empty_like(q)
+    if args.shard == "heads":
+        # head sharding: contiguous blocks of heads per rank, no inter-GPU traffic
+        per = [b_ - a_ for a_, b_ in unit_shards(heads, world)]
+        my_heads = per[rank]
+        grid = vm.TokenGrid(T, h, w, d, my_heads, 1)
+        n = grid.tokens()
+        nq_local = n
+        q = torch.randn((my_heads, n, d), device=dev, dtype=torch.bfloat16, generator=gen)
+        k = torch.randn((my_heads, n, d), device=dev, dtype=torch.bfloat16, generator=gen)
+        v = torch.randn((my_heads, n, d), device=dev, dtype=torch.bfloat16, generator=gen)
+        o = torch.empty_like(q)
+
+        def step(check=False):
+            vm.vmonarch_attention(q, k, v, grid, cfg, out=o, check=check)
+    else:
+        # sequence sharding: every rank holds a spatial slab of all frames for all heads; K/V
+        # are all-gathered over NCCL inside the timed step
+        per = [heads] * world
+        my_heads = heads
+        grid = vm.TokenGrid(T, h, w, d, heads, 1)
+        n = grid.tokens()
+        parts = slab_partition(h * w, world)
+        p0, pc = parts[rank]
+        nq_local = T * pc
+        q = torch.randn((heads, nq_local, d), device=dev, dtype=torch.bfloat16, generator=gen)
+        k = torch.randn((heads, nq_local, d), device=dev, dtype=torch.bfloat16, generator=gen)
+        v = torch.randn((heads, nq_local, d), device=dev, dtype=torch.bfloat16, generator=gen)
+        o = torch.empty_like(q)
+        from paper_2601_22275_b200.dist import vmonarch_attention_seq
+
+        def step(check=False):
+            if world > 1:
+                o.copy_(vmonarch_attention_seq(q, k, v, grid, cfg))
+            else:
+                vm.vmonarch_attention_slab(q, k, v, grid, 0, h * w, cfg, out=o, check=check)
 
     def barrier():
         if world > 1:
@@ -235,9 +266,9 @@ def main():
         return float(t.item())
 
     # ---- device-resident timed region
-    vm.vmonarch_attention(q, k, v, grid, cfg, out=o, check=True)   # validates once (raises on error)
+    step(check=True)   # validates once (raises on error)
     for _ in range(args.warmup):
-        vm.vmonarch_attention(q, k, v, grid, cfg, out=o, check=False)
+        step()
     torch.cuda.synchronize()
     prof_enable = vm.lib.vmb_profile_enable
     prof_enable.argtypes = [C.c_int32]
@@ -256,7 +287,7 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
-        vm.vmonarch_attention(q, k, v, grid, cfg, out=o, check=False)
+        step()
     e1.record()
     torch.cuda.synchronize()
     prof_enable(0)
@@ -277,7 +308,7 @@ def main():
     tflops = total_flops / (ms * 1e-3) / 1e12
     peaks = load_peaks()
     # dominant kernel roofline
-    alg = kernel_algorithmic(grid, my_heads)
+    alg = kernel_algorithmic(grid, my_heads, nq_local / n)
     dom = max((k_ for k_ in kern if k_ in alg), key=lambda k_: kern[k_]["share"], default=None)
     roof = None
     if dom:
@@ -304,7 +335,7 @@ def main():
 
     # ---- end to end through the public API with host buffers
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and args.shard == "heads":
         hq = torch.empty(q.shape, dtype=q.dtype, pin_memory=True)
         hk = torch.empty(k.shape, dtype=k.dtype, pin_memory=True)
         hv = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
@@ -335,7 +366,7 @@ def main():
 
     # ---- dense FlashAttention-style bf16 baseline on the same GPU (same heads)
     dense = None
-    if not args.no_dense:
+    if not args.no_dense and args.shard == "heads" and args.config != "c5":
         od = torch.empty_like(q)
         vm.dense_forward(q[:1], k[:1], v[:1])
         torch.cuda.synchronize()
@@ -352,7 +383,7 @@ def main():
         del od
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config != "c5":
         try:
             cpu = cpu_reference_sample(args.config)
         except Exception as ex:  # noqa
@@ -365,7 +396,7 @@ def main():
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic N(0,1) bf16 Q/K/V (torch.Generator seed 1234+rank), resident in HBM",
             "config": {"workload": desc, "global_heads": heads, "heads_per_gpu": per, "seq_len": n,
-                       "parallelism": f"heads/{world}" if world > 1 else "single GPU",
+                       "parallelism": (f"{args.shard}/{world}" if world > 1 else "single GPU"),
                        "l2": "inputs 1.2 GB per tensor (>126 MB L2); no flush needed"},
             "tflops": round(tflops, 1), "tflops_frac_of_peak": round(tflops / peaks["bf16"], 4),
             "algorithmic_flops_per_call": total_flops,

@@ -109,6 +109,25 @@ vmb_status vmb_export_factors(const vmb_grid* grid, const vmb_config* cfg, vmb_d
                               const void* q, const void* k, const vmb_strides* in_strides,
                               void* workspace, float* L, float* R, void* stream);
 
+/* ---- sequence-sharded mode (multi-GPU) ----
+ * Rank r owns spatial positions [pos_begin, pos_begin + pos_count) of every frame.  Its
+ * queries/outputs are the local slab, contiguous unit-major (units, T * pos_count, d) with
+ * local token = t * pos_count + (position - pos_begin); keys/values are the full tensors
+ * (units, N, d), assembled from the ranks' slabs by one all-gather (NCCL) and
+ * vmb_seq_assemble.  R-step queries, L-step blocks and the first-frame recompute rows are
+ * all slab-local, so this is the only exchange (video.hpp:115-126 per unit).  Default
+ * factorization only; bf16, d = 128, T <= 128. */
+size_t vmb_workspace_size_seq(const vmb_grid* grid, const vmb_config* cfg, vmb_dtype dtype, int64_t pos_count);
+vmb_status vmb_vmonarch_fwd_seq(const vmb_grid* grid, const vmb_config* cfg, vmb_dtype dtype,
+                                int64_t pos_begin, int64_t pos_count, const void* q_local,
+                                const void* k_full, const void* v_full, void* o_local,
+                                void* workspace, size_t workspace_bytes, void* stream);
+/* gathered: `world` blocks of (units, T, slab_max, d) (slab r padded to slab_max rows) ->
+ * full (units, T*h*w, d); rank r's rows land at positions [pos_begin[r], +pos_count[r]). */
+vmb_status vmb_seq_assemble(const vmb_grid* grid, vmb_dtype dtype, int32_t world, const int64_t* pos_begin,
+                            const int64_t* pos_count, int64_t slab_max, const void* gathered, void* full,
+                            void* stream);
+
 /* ---- half steps (monarch.hpp:53-147), unit-major contiguous state tensors ----
  * aR (units,m,b,d) dtype; cR (units,m,b) f32; Kb (units,m,b,d) dtype;
  * aL (units,b,m,d) dtype; cL (units,b,m) f32; Qb (units,b,m,d) dtype (the permuted,

@@ -30,7 +30,7 @@ __all__ = [
     "TokenGrid", "VMonarchConfig", "CostReport", "DimensionError", "DomainError", "StateError",
     "vmonarch_attention", "r_update", "l_update", "flash_entropy_fwd", "dense_forward",
     "factorize", "flops_estimate", "make_perm", "preset_grid", "export_factors", "lib",
-    "kernel_launch_count", "LIB_PATH",
+    "kernel_launch_count", "LIB_PATH", "vmonarch_attention_slab", "seq_assemble",
 ]
 
 LIB_PATH = os.environ.get("VMB_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libvmb.so")
@@ -102,6 +102,10 @@ _vmb_lstep = _sig("vmb_lstep", [_I64, _I64, _I64, _I64, C.c_int, _P, _P, _P, _P,
 _vmb_flash = _sig("vmb_flash_entropy_fwd", [_I64, _I64, _I64, _I64, C.c_int, _P, _P, _P, _F, _P, _P, _P, _P])
 _vmb_dense = _sig("vmb_dense_fwd", [_I64, _I64, _I64, C.c_int, _P, _P, _P, _P, _P])
 _vmb_launches = _sig("vmb_kernel_launch_count", [], C.c_uint64)
+_vmb_ws_size_seq = _sig("vmb_workspace_size_seq", [C.POINTER(_Grid), C.POINTER(_Cfg), C.c_int, _I64], C.c_size_t)
+_vmb_fwd_seq = _sig("vmb_vmonarch_fwd_seq", [C.POINTER(_Grid), C.POINTER(_Cfg), C.c_int, _I64, _I64, _P, _P, _P, _P,
+                                             _P, C.c_size_t, _P])
+_vmb_seq_assemble = _sig("vmb_seq_assemble", [C.POINTER(_Grid), C.c_int, _I32, _P, _P, _I64, _P, _P, _P])
 _vmb_selftest = _sig("vmb_selftest_umma", [_I32, _P, _P, _P, _P])
 
 VMB_F32, VMB_BF16 = 0, 1
@@ -308,6 +312,56 @@ def vmonarch_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, grid: 
                            _ptr(R), st))
         factors_out.clear()
         factors_out.extend((L[u], R[u]) for u in range(U))
+    return out
+
+
+# ----------------------------------------------------------------------------- sequence-sharded mode
+def vmonarch_attention_slab(q_local: torch.Tensor, k_full: torch.Tensor, v_full: torch.Tensor, grid: TokenGrid,
+                            pos_begin: int, pos_count: int, cfg: VMonarchConfig = VMonarchConfig(),
+                            out: Optional[torch.Tensor] = None, check: bool = True) -> torch.Tensor:
+    """The forward for the spatial slab [pos_begin, pos_begin + pos_count) of every frame
+    (SURVEY §8e): q_local / output (units, T * pos_count, d) with local token
+    t * pos_count + (position - pos_begin); k_full, v_full (units, N, d).  Slab outputs of all
+    ranks are exactly the rows of the unsharded forward (queries are row-independent)."""
+    _require_cuda(q_local, k_full, v_full, out)
+    dt = _dtype_code(q_local)
+    U, n, d = grid.units(), grid.tokens(), grid.head_dim
+    nl = grid.t_frames * pos_count
+    if tuple(q_local.shape) != (U, nl, d) or tuple(k_full.shape) != (U, n, d) or tuple(v_full.shape) != (U, n, d):
+        raise DimensionError(f"dimension error: expected q_local ({U}, {nl}, {d}) and k/v ({U}, {n}, {d})")
+    q_local, k_full, v_full = q_local.contiguous(), k_full.contiguous(), v_full.contiguous()
+    if out is None:
+        out = torch.empty_like(q_local)
+    g, c = grid._c(), cfg._c()
+    nbytes = int(_vmb_ws_size_seq(C.byref(g), C.byref(c), dt, pos_count))
+    if nbytes == 0:
+        _check(1)
+    key = (q_local.device, nbytes, "seq")
+    ws = _WS_CACHE.get(key)
+    if ws is None:
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=q_local.device)
+        _WS_CACHE.clear()
+        _WS_CACHE[key] = ws
+    st = _stream()
+    _check(_vmb_fwd_seq(C.byref(g), C.byref(c), dt, pos_begin, pos_count, _ptr(q_local), _ptr(k_full), _ptr(v_full),
+                        _ptr(out), _ptr(ws), ws.numel(), st))
+    if check:
+        _check(_vmb_ws_status(_ptr(ws), st))
+    return out
+
+
+def seq_assemble(gathered: torch.Tensor, grid: TokenGrid, pos_begin: Sequence[int], pos_count: Sequence[int],
+                 out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """(world, units, T, slab_max, d) all-gathered slabs -> (units, N, d) frame-major keys."""
+    _require_cuda(gathered, out)
+    world, U, T, smax, d = gathered.shape
+    if out is None:
+        out = torch.empty((U, grid.tokens(), d), dtype=gathered.dtype, device=gathered.device)
+    b = (C.c_int64 * world)(*pos_begin)
+    cn = (C.c_int64 * world)(*pos_count)
+    g = grid._c()
+    _check(_vmb_seq_assemble(C.byref(g), _dtype_code(gathered), world, C.addressof(b), C.addressof(cn), smax,
+                             _ptr(gathered.contiguous()), _ptr(out), _stream()))
     return out
 
 

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <string>
@@ -238,6 +239,11 @@ struct TcLstepArgs {
     float out_scale;    // multiplies the epilogue (ITER: aR scale)
 };
 void tc_lstep_launch(const TcLstepArgs& a, int64_t U, cudaStream_t s);
+
+// seq_gather.cu: sequence-sharded K/V layout
+constexpr int kMaxSeqRanks = 64;
+void seq_assemble(const void* gathered, void* full, int64_t units, int64_t T, int64_t hw, int64_t slab_max,
+                  int64_t row_bytes, int world, const int64_t* off, const int64_t* cnt, cudaStream_t s);
 
 void selftest_umma(int mode, const void* A, const void* B, float* C, cudaStream_t s);
 

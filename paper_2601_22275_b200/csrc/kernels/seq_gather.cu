@@ -1,0 +1,77 @@
+// seq_gather.cu — layout kernel of the sequence-sharded mode.
+//
+// Rank r owns spatial positions [off_r, off_r + cnt_r) of every frame.  After the NCCL
+// all-gather of K (or V) slabs the buffer holds, per rank, a (units, T, slab_max, d) block
+// (slabs padded to the largest); this kernel scatters those rows into the frame-major
+// (units, T, h*w, d) layout the attention kernels read (token = t*h*w + position).
+// Pure data movement: 16-byte vectors, one warp per row of d elements, HBM-bound.
+#include "../internal.hpp"
+
+namespace vmb {
+namespace {
+
+struct AsmParams {
+    const uint8_t* src;
+    uint8_t* dst;
+    int64_t units, T, hw, slab_max, row_bytes;
+    int32_t world;
+    int64_t off[kMaxSeqRanks];
+    int64_t cnt[kMaxSeqRanks];
+};
+
+__global__ void __launch_bounds__(256) seq_assemble_kernel(const __grid_constant__ AsmParams p) {
+    // one 16-B chunk per thread; grid covers (rank, unit, frame, slab position, chunk)
+    const int64_t chunks = p.row_bytes / 16;
+    const int64_t per_rank = p.units * p.T * p.slab_max * chunks;
+    const int64_t total = per_rank * p.world;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(idx / per_rank);
+        int64_t rest = idx % per_rank;
+        const int64_t c = rest % chunks;
+        rest /= chunks;
+        const int64_t i = rest % p.slab_max;
+        rest /= p.slab_max;
+        const int64_t t = rest % p.T;
+        const int64_t u = rest / p.T;
+        if (i >= p.cnt[r]) continue;  // padding of a short slab
+        const int64_t srow = idx / chunks;  // rows of the gathered buffer: (rank, unit, frame, position)
+        const uint4 v = reinterpret_cast<const uint4*>(p.src + srow * p.row_bytes)[c];
+        const int64_t drow = (u * p.T + t) * p.hw + p.off[r] + i;
+        reinterpret_cast<uint4*>(p.dst + drow * p.row_bytes)[c] = v;
+    }
+}
+
+}  // namespace
+
+void seq_assemble(const void* gathered, void* full, int64_t units, int64_t T, int64_t hw, int64_t slab_max,
+                  int64_t row_bytes, int world, const int64_t* off, const int64_t* cnt, cudaStream_t s) {
+    VMB_REQUIRE_DIM(world >= 1 && world <= kMaxSeqRanks, "sequence-sharded world size out of range");
+    VMB_REQUIRE_DIM(row_bytes % 16 == 0, "row size must be a multiple of 16 bytes");
+    AsmParams p;
+    p.src = static_cast<const uint8_t*>(gathered);
+    p.dst = static_cast<uint8_t*>(full);
+    p.units = units;
+    p.T = T;
+    p.hw = hw;
+    p.slab_max = slab_max;
+    p.row_bytes = row_bytes;
+    p.world = world;
+    for (int r = 0; r < kMaxSeqRanks; ++r) {
+        p.off[r] = r < world ? off[r] : 0;
+        p.cnt[r] = r < world ? cnt[r] : 0;
+        if (r < world) VMB_REQUIRE_DIM(cnt[r] <= slab_max && off[r] + cnt[r] <= hw, "slab outside the frame");
+    }
+    const int64_t total = (int64_t)world * units * T * slab_max * (row_bytes / 16);
+    if (total == 0) return;
+    int dev = 0, sms = 148;
+    VMB_CHECK_CUDA(cudaGetDevice(&dev));
+    VMB_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sms * 16);
+    ProfScope ps(kKSimt, s);
+    seq_assemble_kernel<<<(unsigned)blocks, 256, 0, s>>>(p);
+    count_launch();
+    check_launch("seq_assemble");
+}
+
+}  // namespace vmb

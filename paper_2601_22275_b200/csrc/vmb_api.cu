@@ -205,6 +205,9 @@ void attn_launch(const Tc2Args& a, int64_t U, cudaStream_t s, bool rstep) {
 struct Shape {
     int64_t T, h, w, d, H, B, U, N, m, b, hw;
     bool recompute;
+    // query-side extent: all b positions (bq == b, Nq == N, hwq == hw) or, in the
+    // sequence-sharded mode, a slab of bq spatial positions of every frame
+    int64_t bq = 0, Nq = 0, hwq = 0;
 };
 
 Shape make_shape(const vmb_grid* g, const vmb_config* c) {
@@ -233,6 +236,9 @@ Shape make_shape(const vmb_grid* g, const vmb_config* c) {
         s.m = s.T;
         s.b = s.hw;
     }
+    s.bq = s.b;
+    s.Nq = s.N;
+    s.hwq = s.hw;
     return s;
 }
 
@@ -251,8 +257,8 @@ struct Workspace {
 
 Workspace carve(void* base, const Shape& s, vmb_dtype dt) {
     const size_t es = dt == VMB_BF16 ? 2 : 4;
-    const size_t act = align_up((size_t)s.U * s.N * s.d * es);
-    const size_t st = align_up((size_t)s.U * s.N * sizeof(float));
+    const size_t act = align_up((size_t)s.U * s.Nq * s.d * es);
+    const size_t st = align_up((size_t)s.U * s.Nq * sizeof(float));
     uint8_t* p = static_cast<uint8_t*>(base);
     Workspace w;
     w.status = reinterpret_cast<int32_t*>(p);
@@ -265,12 +271,12 @@ Workspace carve(void* base, const Shape& s, vmb_dtype dt) {
     w.part_o = w.part_lse = nullptr;
     w.nsplit = 1;
     if (dt == VMB_BF16 && s.d == 128 && s.recompute && s.U > 0) {
-        w.nsplit = attn_plan_splits(s.hw, s.N, s.U);
+        w.nsplit = attn_plan_splits(s.hwq, s.N, s.U);
         if (w.nsplit > 1) {
             w.part_o = reinterpret_cast<float*>(p + off);
-            off += align_up((size_t)s.U * w.nsplit * s.hw * 128 * sizeof(float));
+            off += align_up((size_t)s.U * w.nsplit * s.hwq * 128 * sizeof(float));
             w.part_lse = reinterpret_cast<float*>(p + off);
-            off += align_up((size_t)s.U * w.nsplit * s.hw * sizeof(float));
+            off += align_up((size_t)s.U * w.nsplit * s.hwq * sizeof(float));
         }
     }
     w.bytes = off;
@@ -367,30 +373,34 @@ vmb_status guarded(F&& f) {
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 // ---------------------------------------------------------------- the forward plan
+// in: strides of q; kin: strides of k and v; out: strides of o.  Queries/outputs cover s.bq
+// positions of every frame (s.bq == s.b except in the sequence-sharded mode); keys/values
+// cover all s.b positions.
 void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q, const void* k,
-             const void* v, void* o, const vmb_strides& in, const vmb_strides& out, const Workspace& ws,
-             cudaStream_t st) {
+             const void* v, void* o, const vmb_strides& in, const vmb_strides& kin, const vmb_strides& out,
+             const Workspace& ws, cudaStream_t st) {
     const bool bf16 = dt == VMB_BF16;
     const float qscale = (float)(1.0 / std::sqrt((double)s.d));
     const bool recompute = cfg.recompute_first_frame != 0;
     const bool skip_j0 = recompute && s.b == s.hw;
-    const int64_t U = s.U, m = s.m, b = s.b, d = s.d;
+    const int64_t U = s.U, m = s.m, b = s.b, d = s.d, bq = s.bq;
     VMB_CHECK_CUDA(cudaMemsetAsync(ws.status, 0, sizeof(int32_t), st));
     if (U == 0) return;
+    const bool sharded = bq != b;
 
-    if (tc_eligible(s, dt, in, out, q, k, v, o)) {
+    if (tc_eligible(s, dt, in, out, q, k, v, o) && tc_eligible(s, dt, kin, out, q, k, v, o)) {
         // ------------------------------------------------ tcgen05 path
-        const CUtensorMap mQrow = user_map(q, in, s, b, 1, m, b, 128, 1);    // (d, i, k): query tiles
-        const CUtensorMap mK = user_map(k, in, s, b, 1, m, b, 128, 1);
-        const CUtensorMap mV = user_map(v, in, s, b, 1, m, b, 128, 1);
-        const CUtensorMap mK2 = user_map(k, in, s, b, 1, m, b, attn_kv_box(true), 1);  // attention key tiles
+        const CUtensorMap mQrow = user_map(q, in, s, bq, 1, m, bq, 128, 1);    // (d, i, k): query tiles
+        const CUtensorMap mK = user_map(k, kin, s, b, 1, m, b, 128, 1);
+        const CUtensorMap mV = user_map(v, kin, s, b, 1, m, b, 128, 1);
+        const CUtensorMap mK2 = user_map(k, kin, s, b, 1, m, b, attn_kv_box(true), 1);  // attention key tiles
         const uint32_t lrows = (uint32_t)lstep_rows(m);
-        const CUtensorMap mQcol = user_map(q, in, s, b, 1, m, b, 1, lrows);   // (d, i, j): Qb[i] boxes
-        const CUtensorMap mAR = internal_map(ws.aR, U, m, b, d, true, 128, 1);  // aR (U,m,b,d): (d,i,k) query tiles
-        const CUtensorMap mARst = internal_map(ws.aR, U, m, b, d, true, 1, lrows);  // aR columns (d,i,k) for the L-step store
-        const CUtensorMap mAL = internal_map(ws.aL, U, b, m, d, true, lrows, 1);  // aL (U,b,m,d): (d,k,i)
-        const CUtensorMap mY = internal_map(ws.y, U, m, b, d, true, 1, lrows);    // y (U,m,b,d): (d,i,k)
-        const CUtensorMap mOcol = user_map(o, out, s, b, 1, m, b, 1, lrows);  // O rows j*b+i: (d, i, j)
+        const CUtensorMap mQcol = user_map(q, in, s, bq, 1, m, bq, 1, lrows);   // (d, i, j): Qb[i] boxes
+        const CUtensorMap mAR = internal_map(ws.aR, U, m, bq, d, true, 128, 1);  // aR (U,m,bq,d): (d,i,k) query tiles
+        const CUtensorMap mARst = internal_map(ws.aR, U, m, bq, d, true, 1, lrows);  // aR columns (d,i,k), L-step store
+        const CUtensorMap mAL = internal_map(ws.aL, U, bq, m, d, true, lrows, 1);  // aL (U,bq,m,d): (d,k,i)
+        const CUtensorMap mY = internal_map(ws.y, U, m, bq, d, true, 1, lrows);    // y (U,m,bq,d): (d,i,k)
+        const CUtensorMap mOcol = user_map(o, out, s, bq, 1, m, bq, 1, lrows);  // O rows j*bq+i: (d, i, j)
         for (int64_t t = 0; t < cfg.iters; ++t) {
             const bool last = t == cfg.iters - 1;
             TcFaArgs fa{};
@@ -398,7 +408,7 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
             fa.tmK = mK;
             fa.tmV = mV;
             fa.nseg = (int32_t)m;
-            fa.q_len = (int32_t)b;
+            fa.q_len = (int32_t)bq;
             fa.kv_len = (int32_t)b;
             fa.qH = t == 0 ? (int32_t)std::max<int64_t>(s.H, 1) : 1;
             fa.kH = (int32_t)std::max<int64_t>(s.H, 1);
@@ -409,10 +419,10 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
             fa.clamp_enabled = cfg.clamp_enabled;
             fa.nv = last ? 2 : 1;
             fa.v_is_k = last ? 0 : 1;
-            fa.out0 = ws.aL;                       // aL (U, b, m, d): row (u, k, i)
-            fa.oB[0] = b * m * d; fa.oH[0] = 0; fa.oS[0] = d; fa.oR[0] = m * d;
-            fa.out1 = ws.y;                        // y (U, m, b, d): row (u, k, i)
-            fa.oB[1] = m * b * d; fa.oH[1] = 0; fa.oS[1] = b * d; fa.oR[1] = d;
+            fa.out0 = ws.aL;                       // aL (U, bq, m, d): row (u, k, i)
+            fa.oB[0] = bq * m * d; fa.oH[0] = 0; fa.oS[0] = d; fa.oR[0] = m * d;
+            fa.out1 = ws.y;                        // y (U, m, bq, d): row (u, k, i)
+            fa.oB[1] = m * bq * d; fa.oH[1] = 0; fa.oS[1] = bq * d; fa.oR[1] = d;
             fa.cl_out = ws.cL;
             fa.lse_out = nullptr;
             fa.status = ws.status;
@@ -439,7 +449,7 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
                 f2.clamp_enabled = fa.clamp_enabled;
                 f2.nv = 1;
                 f2.out = ws.aL;
-                f2.oB = b * m * d; f2.oH = 0; f2.oS = d; f2.oR = m * d;
+                f2.oB = bq * m * d; f2.oH = 0; f2.oS = d; f2.oR = m * d;
                 f2.cl_out = ws.cL;
                 f2.status = ws.status;
                 f2.check_finite = fa.check_finite;
@@ -455,7 +465,7 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
             ls.cL = ws.cL;
             ls.qscale = qscale;
             ls.m = (int32_t)m;
-            ls.b = (int32_t)b;
+            ls.b = (int32_t)bq;
             ls.H = (int32_t)std::max<int64_t>(s.H, 1);
             ls.oHn = (int32_t)std::max<int64_t>(s.H, 1);
             ls.final_mode = last;
@@ -468,11 +478,11 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
             const int64_t Hm = std::max<int64_t>(s.H, 1);
             const uint32_t bn = attn_kv_box(false);
             Tc2Args f2{};
-            f2.tmQ = user_map(q, in, s, s.hw, 1, 1, s.hw, 128, 1);
-            f2.tmK = user_map(k, in, s, s.N, 1, 1, s.N, bn, 1);
-            f2.tmV = user_map(v, in, s, s.N, 1, 1, s.N, bn, 1);
+            f2.tmQ = user_map(q, in, s, s.hwq, 1, 1, s.hwq, 128, 1);
+            f2.tmK = user_map(k, kin, s, s.N, 1, 1, s.N, bn, 1);
+            f2.tmV = user_map(v, kin, s, s.N, 1, 1, s.N, bn, 1);
             f2.nseg = 1;
-            f2.q_len = (int32_t)s.hw;
+            f2.q_len = (int32_t)s.hwq;
             f2.kv_len = (int32_t)s.N;
             f2.qH = f2.kH = f2.oHn = (int32_t)Hm;
             f2.qscale = qscale;
@@ -489,6 +499,7 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
     }
 
     // ---------------------------------------------------- CUDA-core path (any shape / fp32)
+    VMB_REQUIRE_DIM(!sharded, "the sequence-sharded mode needs the tcgen05 path (bf16, d = 128, m <= 128)");
     check_finite_rows(user_view(q, in, s, 0, 1), U, s.N, d, bf16, ws.status, st);
     const View vQrow = user_view(q, in, s, b, 1);    // (u, k, i) -> token k*b+i
     const View vK = user_view(k, in, s, b, 1);
@@ -655,7 +666,64 @@ vmb_status vmb_vmonarch_fwd(const vmb_grid* grid, const vmb_config* cfg, vmb_dty
         const Workspace ws = carve(workspace, s, dtype);
         VMB_REQUIRE_DIM(workspace != nullptr && ws_bytes >= ws.bytes, "workspace too small");
         VMB_REQUIRE_DIM(s.U == 0 || (q && k && v && o), "null tensor pointer");
-        forward(s, *cfg, dtype, q, k, v, o, *in, *out, ws, as_stream(stream));
+        forward(s, *cfg, dtype, q, k, v, o, *in, *in, *out, ws, as_stream(stream));
+    });
+}
+
+// ---- sequence-sharded mode ----
+namespace {
+Shape seq_shape(const vmb_grid* grid, const vmb_config* cfg, int64_t pos_begin, int64_t pos_count) {
+    Shape s = make_shape(grid, cfg);
+    VMB_REQUIRE_DIM(cfg->override_m == 0 && cfg->override_b == 0,
+                    "the sequence-sharded mode uses the default factorization (m, b) = (T, h*w)");
+    VMB_REQUIRE_DIM(pos_begin >= 0 && pos_count >= 1 && pos_begin + pos_count <= s.hw,
+                    "spatial slab outside the frame");
+    s.bq = pos_count;
+    s.Nq = s.m * pos_count;
+    s.hwq = pos_count;
+    return s;
+}
+}  // namespace
+
+size_t vmb_workspace_size_seq(const vmb_grid* grid, const vmb_config* cfg, vmb_dtype dtype, int64_t pos_count) {
+    try {
+        const Shape s = seq_shape(grid, cfg, 0, pos_count);
+        return carve(nullptr, s, dtype).bytes;
+    } catch (const Error& e) {
+        set_error(e.msg);
+        return 0;
+    }
+}
+
+vmb_status vmb_vmonarch_fwd_seq(const vmb_grid* grid, const vmb_config* cfg, vmb_dtype dtype, int64_t pos_begin,
+                                int64_t pos_count, const void* q_local, const void* k_full, const void* v_full,
+                                void* o_local, void* workspace, size_t ws_bytes, void* stream) {
+    return guarded([&] {
+        const Shape s = seq_shape(grid, cfg, pos_begin, pos_count);
+        VMB_REQUIRE_DIM(dtype == VMB_BF16 && s.d == 128 && s.m <= 128,
+                        "the sequence-sharded mode needs bf16, d = 128 and T <= 128");
+        const Workspace ws = carve(workspace, s, dtype);
+        VMB_REQUIRE_DIM(workspace != nullptr && ws_bytes >= ws.bytes, "workspace too small");
+        VMB_REQUIRE_DIM(s.U == 0 || (q_local && k_full && v_full && o_local), "null tensor pointer");
+        vmb_strides local, full;
+        local.token = full.token = s.d;
+        local.head = s.Nq * s.d;
+        local.batch = s.H * s.Nq * s.d;
+        full.head = s.N * s.d;
+        full.batch = s.H * s.N * s.d;
+        forward(s, *cfg, dtype, q_local, k_full, v_full, o_local, local, full, local, ws, as_stream(stream));
+    });
+}
+
+vmb_status vmb_seq_assemble(const vmb_grid* grid, vmb_dtype dtype, int32_t world, const int64_t* pos_begin,
+                            const int64_t* pos_count, int64_t slab_max, const void* gathered, void* full,
+                            void* stream) {
+    return guarded([&] {
+        VMB_REQUIRE_DIM(grid && pos_begin && pos_count, "null argument");
+        const int64_t units = grid->heads * grid->batch, hw = grid->h * grid->w;
+        const int64_t es = dtype == VMB_BF16 ? 2 : 4;
+        seq_assemble(gathered, full, units, grid->t_frames, hw, slab_max, grid->head_dim * es, world, pos_begin,
+                     pos_count, as_stream(stream));
     });
 }
 

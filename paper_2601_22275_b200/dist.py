@@ -39,3 +39,55 @@ def gather_units(local, units: int, group=None):
     bufs = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(bufs, pad, group=group)
     return torch.cat([buf[: b - a] for buf, (a, b) in zip(bufs, shards)], dim=0)
+
+
+# ----------------------------------------------------------------------------- sequence sharding
+def slab_partition(positions: int, world: int) -> List[Tuple[int, int]]:
+    """(begin, count) of each rank's spatial slab: contiguous, sizes differ by at most one."""
+    return [(a, b - a) for a, b in unit_shards(positions, world)]
+
+
+def local_slab(x, grid, begin: int, count: int):
+    """Rank-local slab of a full (units, N, d) tensor: (units, T * count, d), token t*count + i."""
+    U, n, d = x.shape
+    hw = grid.h * grid.w
+    return x.view(U, grid.t_frames, hw, d)[:, :, begin:begin + count].reshape(U, grid.t_frames * count, d)
+
+
+def gather_slabs(x_local, grid, group=None):
+    """all_gather the ranks' (units, T*count_r, d) slabs into (world, units, T, slab_max, d)
+    (slabs zero-padded to the largest): the one collective of the sequence-sharded mode."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    parts = slab_partition(grid.h * grid.w, world)
+    smax = max(c for _, c in parts)
+    U, nl, d = x_local.shape
+    cnt = nl // grid.t_frames
+    send = x_local.new_zeros((U, grid.t_frames, smax, d))
+    send[:, :, :cnt] = x_local.view(U, grid.t_frames, cnt, d)
+    recv = x_local.new_empty((world * U, grid.t_frames, smax, d))
+    dist.all_gather_into_tensor(recv, send, group=group)
+    return recv.view(world, U, grid.t_frames, smax, d), parts, smax
+
+
+def vmonarch_attention_seq(q_local, k_local, v_local, grid, cfg=None, group=None):
+    """Sequence-sharded VMonarch forward: every rank holds the slab
+    slab_partition(h*w, world)[rank] of all frames for Q, K, V; K and V are all-gathered over
+    NCCL (one exchange per call) and assembled into frame-major order by a libvmb kernel; the
+    forward then runs on the local query slab.  Returns the local output slab."""
+    import torch.distributed as dist
+
+    import paper_2601_22275_b200 as vm
+
+    cfg = cfg or vm.VMonarchConfig()
+    rank = dist.get_rank(group)
+    kg, parts, _ = gather_slabs(k_local, grid, group)
+    vg, _, _ = gather_slabs(v_local, grid, group)
+    begins = [a for a, _ in parts]
+    counts = [c for _, c in parts]
+    k_full = vm.seq_assemble(kg, grid, begins, counts)
+    v_full = vm.seq_assemble(vg, grid, begins, counts)
+    b0, cnt = parts[rank]
+    return vm.vmonarch_attention_slab(q_local, k_full, v_full, grid, b0, cnt, cfg, check=False)

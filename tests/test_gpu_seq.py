@@ -1,0 +1,71 @@
+"""GPU: the sequence-sharded mode simulated on one B200.
+
+For W ranks the slabs of slab_partition(h*w, W) are run one after another on the same device
+through vmb_vmonarch_fwd_seq (the per-rank call of dist.vmonarch_attention_seq), with K/V
+assembled from padded slabs by vmb_seq_assemble (the layout step after the NCCL
+all-gather).  Query rows are independent, so the stitched slab outputs must equal the
+unsharded forward: the R/L half-steps bitwise, the first-frame rows (split-KV recompute
+whose split count depends on the slab) to fp32-combine rounding."""
+import numpy as np
+import pytest
+import torch
+
+from oracle.oracle import bf16_round, workload
+from vmb_testutil import relfro
+
+pytestmark = pytest.mark.gpu
+
+
+def _slabs(vm, grid, x, parts):
+    from paper_2601_22275_b200.dist import local_slab
+    return [local_slab(x, grid, a, c) for a, c in parts]
+
+
+@pytest.mark.parametrize("gridt,heads,world", [((4, 8, 16), 2, 2), ((5, 6, 20), 3, 3), ((21, 30, 52), 1, 8)])
+def test_seq_assemble_is_exact(vm, cuda, gridt, heads, world):
+    from paper_2601_22275_b200.dist import slab_partition
+    grid = vm.TokenGrid(*gridt, 128, heads, 1)
+    g = torch.Generator(device=cuda).manual_seed(5)
+    k = torch.randn((heads, grid.tokens(), 128), device=cuda, generator=g).to(torch.bfloat16)
+    parts = slab_partition(grid.h * grid.w, world)
+    smax = max(c for _, c in parts)
+    gathered = torch.zeros((world, heads, grid.t_frames, smax, 128), device=cuda, dtype=torch.bfloat16)
+    for r, s in enumerate(_slabs(vm, grid, k, parts)):
+        gathered[r, :, :, :parts[r][1]] = s.view(heads, grid.t_frames, parts[r][1], 128)
+    full = vm.seq_assemble(gathered, grid, [a for a, _ in parts], [c for _, c in parts])
+    torch.cuda.synchronize()
+    assert torch.equal(full, k)
+
+
+@pytest.mark.parametrize("gridt,heads,world", [((4, 8, 16), 2, 2), ((6, 10, 26), 2, 3), ((21, 30, 52), 1, 8)])
+def test_seq_sharded_forward_equals_unsharded(vm, cuda, gridt, heads, world):
+    from paper_2601_22275_b200.dist import local_slab, slab_partition
+    grid = vm.TokenGrid(*gridt, 128, heads, 1)
+    cfg = vm.VMonarchConfig()
+    q, k, v = workload(heads, grid.tokens(), 128, seed=21)
+    tq, tk, tv = (torch.from_numpy(bf16_round(x)).to(cuda, torch.bfloat16) for x in (q, k, v))
+    full = vm.vmonarch_attention(tq, tk, tv, grid, cfg)
+    parts = slab_partition(grid.h * grid.w, world)
+    T, hw = grid.t_frames, grid.h * grid.w
+    stitched = torch.empty_like(full).view(heads, T, hw, 128)
+    for a, c in parts:
+        o = vm.vmonarch_attention_slab(local_slab(tq, grid, a, c), tk, tv, grid, a, c, cfg)
+        stitched[:, :, a:a + c] = o.view(heads, T, c, 128)
+    torch.cuda.synchronize()
+    stitched = stitched.view_as(full)
+    f, s = full.float().view(heads, T, hw, 128), stitched.float().view(heads, T, hw, 128)
+    # frames >= 1: R/L half-steps only, row-local -> bitwise
+    assert torch.equal(f[:, 1:], s[:, 1:])
+    # frame 0: first-frame recompute rows (split-KV combine order may differ with the slab)
+    assert relfro(s[:, 0].cpu().numpy(), f[:, 0].cpu().numpy()) <= 2e-3
+
+
+def test_seq_slab_validation(vm, cuda):
+    grid = vm.TokenGrid(4, 8, 16, 128, 1, 1)
+    x = torch.zeros((1, grid.tokens(), 128), device=cuda, dtype=torch.bfloat16)
+    with pytest.raises(vm.DimensionError):
+        vm.vmonarch_attention_slab(torch.zeros((1, 4 * 10, 128), device=cuda, dtype=torch.bfloat16), x, x, grid,
+                                   120, 10)
+    with pytest.raises(vm.DimensionError):
+        vm.vmonarch_attention_slab(torch.zeros((1, 4 * 10, 128), device=cuda, dtype=torch.float32), x.float(),
+                                   x.float(), grid, 0, 10)
