@@ -1,0 +1,126 @@
+// dropin_test.cpp — the drop-in check of include/vmonarch_b200.hpp against the UNMODIFIED
+// reference operator.  TEST INFRASTRUCTURE ONLY (built by oracle/Makefile into oracle/_ref/
+// from the reference's own headers and sources under /root/reference/proj; run on a GPU box
+// by tests/test_gpu_dropin.py).
+//
+// The same vmonarch::Mat<float> / TokenGrid / VMonarchConfig / MonarchFactors<float> objects
+// go to both calls:
+//     vmonarch::vmonarch_attention<float>(qs, ks, vs, grid, cfg, threads, &factors)  (CPU)
+//     vmonarch_b200::vmonarch_attention(qs, ks, vs, grid, cfg, threads, &factors)    (B200)
+// and the outputs, the factors and the exception types must agree (fp32 parity <= 1e-4).
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "vmonarch/video.hpp"
+#include "vmonarch_b200.hpp"
+
+using vmonarch::Mat;
+
+static std::vector<Mat<float>> randn_units(int units, long rows, long cols, uint64_t seed, double sigma) {
+    std::vector<Mat<float>> out;
+    for (int u = 0; u < units; ++u) {
+        std::mt19937_64 rng(seed + 3 * u);
+        std::normal_distribution<double> nd(0.0, 1.0);
+        Mat<float> m(rows, cols);
+        for (auto& x : m.data) x = static_cast<float>(sigma * nd(rng));
+        out.push_back(std::move(m));
+    }
+    return out;
+}
+
+static double relfro(const std::vector<float>& a, const std::vector<float>& b) {
+    double num = 0, den = 0;
+    for (size_t i = 0; i < a.size(); ++i) {
+        num += (double(a[i]) - b[i]) * (double(a[i]) - b[i]);
+        den += double(b[i]) * b[i];
+    }
+    return std::sqrt(num / (den > 0 ? den : 1e-300));
+}
+
+static int failures = 0;
+static void expect(bool ok, const std::string& what) {
+    std::printf("[%s] %s\n", ok ? "PASS" : "FAIL", what.c_str());
+    if (!ok) ++failures;
+}
+
+static void parity_case(const char* name, vmonarch::TokenGrid grid, vmonarch::VMonarchConfig cfg, double sigma,
+                        bool factors) {
+    const long n = grid.tokens();
+    auto qs = randn_units((int)grid.units(), n, grid.head_dim, 100, sigma);
+    auto ks = randn_units((int)grid.units(), n, grid.head_dim, 101, sigma);
+    auto vs = randn_units((int)grid.units(), n, grid.head_dim, 102, sigma);
+    std::span<const Mat<float>> sq(qs), sk(ks), sv(vs);
+    std::vector<vmonarch::MonarchFactors<float>> fr, fg;
+    auto ref = vmonarch::vmonarch_attention<float>(sq, sk, sv, grid, cfg, 4, factors ? &fr : nullptr);
+    auto got = vmonarch_b200::vmonarch_attention(sq, sk, sv, grid, cfg, 4, factors ? &fg : nullptr);
+    double worst = 0;
+    for (size_t u = 0; u < ref.size(); ++u) worst = std::max(worst, relfro(got[u].data, ref[u].data));
+    char buf[256];
+    std::snprintf(buf, sizeof buf, "%s: output rel-Fro %.2e (<= 1e-4)", name, worst);
+    expect(got.size() == ref.size() && worst <= 1e-4, buf);
+    if (factors) {
+        double wl = 0, wr = 0;
+        for (size_t u = 0; u < fr.size(); ++u) {
+            wl = std::max(wl, relfro(fg[u].L.data, fr[u].L.data));
+            wr = std::max(wr, relfro(fg[u].R.data, fr[u].R.data));
+        }
+        std::snprintf(buf, sizeof buf, "%s: factors L %.2e R %.2e (<= 1e-4)", name, wl, wr);
+        expect(fg.size() == fr.size() && wl <= 1e-4 && wr <= 1e-4, buf);
+    }
+}
+
+template <class E, class F>
+static bool throws(F&& f) {
+    try {
+        f();
+    } catch (const E&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+int main() {
+    // C1 (BASELINE configs[0]): B=1 H=2 d=64, 4 frames x 8x8, fp32, t=3
+    vmonarch::TokenGrid c1{4, 8, 8, 64, 2, 1};
+    vmonarch::VMonarchConfig cfg3;
+    cfg3.iters = 3;
+    parity_case("C1", c1, cfg3, 1.0, true);
+    vmonarch::VMonarchConfig norec;
+    norec.recompute_first_frame = false;
+    parity_case("C1 without first-frame recompute, t=2", c1, norec, 1.0, true);
+    vmonarch::VMonarchConfig ov;
+    ov.override_m_b = std::make_pair(8L, 32L);
+    parity_case("override factorization (m,b)=(8,32)", c1, ov, 1.0, false);
+    vmonarch::VMonarchConfig noclamp;
+    noclamp.clamp_enabled = false;
+    parity_case("clamp disabled, sigma=2", vmonarch::TokenGrid{3, 6, 5, 32, 3, 1}, noclamp, 2.0, false);
+    parity_case("batch 2 x heads 2, d=16", vmonarch::TokenGrid{5, 4, 4, 16, 2, 2}, vmonarch::VMonarchConfig{}, 3.0,
+                false);
+
+    // error contract (check.hpp:10-20): same exception classes as the reference
+    auto qs = randn_units(2, 256, 64, 7, 1.0);
+    auto ks = randn_units(2, 256, 64, 8, 1.0);
+    auto vs = randn_units(2, 256, 64, 9, 1.0);
+    std::span<const Mat<float>> sq(qs), sk(ks), sv(vs);
+    std::span<const Mat<float>> sq1(qs.data(), 1);
+    expect(throws<std::invalid_argument>([&] { vmonarch::vmonarch_attention<float>(sq1, sk, sv, c1, cfg3); }) &&
+               throws<std::invalid_argument>([&] { vmonarch_b200::vmonarch_attention(sq1, sk, sv, c1, cfg3); }),
+           "unit-count mismatch -> std::invalid_argument in both");
+    vmonarch::VMonarchConfig badov;
+    badov.override_m_b = std::make_pair(7L, 37L);
+    expect(throws<std::invalid_argument>([&] { vmonarch::vmonarch_attention<float>(sq, sk, sv, c1, badov); }) &&
+               throws<std::invalid_argument>([&] { vmonarch_b200::vmonarch_attention(sq, sk, sv, c1, badov); }),
+           "override with m*b != N -> std::invalid_argument in both");
+    qs[1].data[17] = NAN;
+    expect(throws<std::domain_error>([&] { vmonarch::vmonarch_attention<float>(sq, sk, sv, c1, cfg3); }) &&
+               throws<std::domain_error>([&] { vmonarch_b200::vmonarch_attention(sq, sk, sv, c1, cfg3); }),
+           "non-finite Q -> std::domain_error in both");
+    std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "OK", failures);
+    return failures ? 1 : 0;
+}
