@@ -214,6 +214,11 @@ struct Tc4Args {
     float* part_lse;
     int32_t max_split;
     int32_t nsplit;              // set by the launcher
+    // query rows for the epilogue's entropy dot (cl_out): row (u, s, r) at
+    // q_rows + (u/qrHn)*qrB + (u%qrHn)*qrH + s*qrS + r*qrR (bf16)
+    const void* q_rows;
+    int64_t qrB, qrH, qrS, qrR;
+    int32_t qrHn;
 };
 int tc4_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg, int max_split);
 void tc4_fa_launch(Tc4Args a, int64_t U, cudaStream_t s);

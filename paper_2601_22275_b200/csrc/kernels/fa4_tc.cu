@@ -23,7 +23,9 @@
 // TMEM (512 columns): S0 [0,128), S1 [128,256) double-buffered scores (P written back as
 // bf16 over the first 64 columns); NO=1: O0 [256,384), O1 [384,512) double-buffered over
 // items; NO=2: O [256,512) = [P K | P V].
-// Shared memory: Q double-buffered over items (2 x 32 KB) + the K (or K|V) ring.
+// Shared memory: one Q tile (released by the MMA warp after the item's last S MMA, so the
+// next item's Q load overlaps the last tile's softmax / PV) + a 6-stage K (or 3-stage K|V)
+// ring.  The epilogue's entropy dot reads the q row from global memory (L2).
 //
 // Issue order (flattened tile index g over this CTA's items): S(g), PV(g-1), S(g+1), ...
 // S(g) goes to buffer g&1 after PV(g-2) has been issued (in-order tcgen05 pipeline), and
@@ -115,19 +117,20 @@ __device__ __forceinline__ Item decode(const Params& p, int64_t it) {
 
 template <int NB>
 struct Smem {
-    static constexpr int S = NB == 1 ? 4 : 2;             // KV stages
-    static constexpr uint32_t q_off = 0;                  // 2 Q buffers
-    static constexpr uint32_t kv_off = 2 * kTileBytes;
+    static constexpr int S = NB == 1 ? 5 : 3;             // KV stages (32 KB K or 64 KB K|V each)
+    static constexpr uint32_t q_off = 0;                  // one Q buffer, released by the MMA warp
+    static constexpr uint32_t kv_off = kTileBytes;        // after the item's last S
     static constexpr uint32_t bar_off = kv_off + S * NB * kTileBytes;
-    // q_full[2], q_empty[2], kv_full[S], kv_empty[S], s_full[2], p_full[2], pv_done,
-    // o_full[2], o_empty[2]
-    static constexpr uint32_t n_bars = 4 + 2 * S + 5 + 4;
+    // q_full, q_empty, kv_full[S], kv_empty[S], s_full[2], p_full[2], pv_done, o_full[2],
+    // o_empty[2]
+    static constexpr uint32_t n_bars = 2 + 2 * S + 5 + 4;
     static constexpr uint32_t slot_off = bar_off + n_bars * 8;
-    // float [4 slots][2 halves][128 rows]: slots 0/1 per-tile max (double-buffered), 2 row
-    // sum and 3 entropy dot of the epilogue
+    // float [2 slots][2 halves][128 rows]: per-tile max exchange (double-buffered); the
+    // epilogue's row-sum / entropy exchanges reuse a slot behind a trailing barrier
     static constexpr uint32_t xch_off = slot_off + 16;
-    static constexpr uint32_t bytes = xch_off + 4 * 2 * 128 * 4;
-    static constexpr uint32_t alloc = bytes + 1024;
+    static constexpr uint32_t bytes = xch_off + 2 * 2 * 128 * 4;
+    // the dynamic smem window starts 1024-aligned (checked in the kernel): no slack needed
+    static constexpr uint32_t alloc = bytes;
 };
 
 template <int NB, int NO>
@@ -136,11 +139,12 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
     constexpr int S = SM::S;
     constexpr int NOB = NO == 1 ? 2 : 1;  // O buffers
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = smem_raw;
+    if (smem_u32(smem_raw) & 1023u) __trap();  // SW128 operand tiles need 1024-B alignment
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::bar_off);
-    uint64_t* q_full = bars;              // [2]
-    uint64_t* q_empty = bars + 2;         // [2]
-    uint64_t* kv_full = bars + 4;         // [S]
+    uint64_t* q_full = bars;
+    uint64_t* q_empty = bars + 1;
+    uint64_t* kv_full = bars + 2;         // [S]
     uint64_t* kv_empty = kv_full + S;     // [S]
     uint64_t* s_full = kv_empty + S;      // [2]
     uint64_t* p_full = s_full + 2;        // [2]
@@ -156,9 +160,9 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
         tma_prefetch_desc(&a.tmQ);
         tma_prefetch_desc(&a.tmK);
         if (NB == 2) tma_prefetch_desc(&a.tmV);
+        mbar_init(q_full, 1);
+        mbar_init(q_empty, 1);
         for (int i = 0; i < 2; ++i) {
-            mbar_init(&q_full[i], 1);
-            mbar_init(&q_empty[i], 256);
             mbar_init(&s_full[i], 1);
             mbar_init(&p_full[i], 256);
             mbar_init(&o_full[i], 1);
@@ -185,14 +189,14 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
             int n = 0;
             for (int64_t it = blockIdx.x; it < p.n_items; it += gridDim.x, ++n) {
                 const Item w = decode(p, it);
-                const int qbuf = n & 1;
-                if (n >= 2) mbar_wait_sleep(&q_empty[qbuf], ((n >> 1) - 1) & 1);
+                // the Q buffer frees once the previous item's last S MMA has completed
+                if (n >= 1) mbar_wait_sleep(q_empty, (n - 1) & 1);
                 const int qb = w.u / a.qH, qh = w.u % a.qH;
                 const int kb = w.u / a.kH, kh = w.u % a.kH;
-                uint8_t* sq = smem + SM::q_off + qbuf * kTileBytes;
-                mbar_arrive_expect_tx(&q_full[qbuf], kTileBytes);
-                tma_load_5d(sq, &a.tmQ, &q_full[qbuf], 0, w.qtile * kTile, w.seg, qh, qb);
-                tma_load_5d(sq + kPanel, &a.tmQ, &q_full[qbuf], 64, w.qtile * kTile, w.seg, qh, qb);
+                uint8_t* sq = smem + SM::q_off;
+                mbar_arrive_expect_tx(q_full, kTileBytes);
+                tma_load_5d(sq, &a.tmQ, q_full, 0, w.qtile * kTile, w.seg, qh, qb);
+                tma_load_5d(sq + kPanel, &a.tmQ, q_full, 64, w.qtile * kTile, w.seg, qh, qb);
                 for (int j = 0; j < w.n_kv; ++j, ++g) {
                     const int st = (int)(g % S);
                     if (g >= S) mbar_wait_sleep(&kv_empty[st], ((g / S) - 1) & 1);
@@ -238,9 +242,8 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
             int n = 0;
             for (int64_t it = blockIdx.x; it < p.n_items; it += gridDim.x, ++n) {
                 const Item w = decode(p, it);
-                const int qbuf = n & 1;
-                mbar_wait_sleep(&q_full[qbuf], (n >> 1) & 1);
-                const uint32_t qa = q_addr + qbuf * kTileBytes;
+                mbar_wait_sleep(q_full, n & 1);
+                const uint32_t qa = q_addr;
                 for (int j = 0; j < w.n_kv; ++j, ++g) {
                     const int st = (int)(g % S);
                     mbar_wait_sleep(&kv_full[st], (g / S) & 1);
@@ -253,6 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                         umma_ss(tS, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(kaddr + off, 16, 1024), idS, kk > 0);
                     }
                     umma_commit(&s_full[g & 1]);
+                    if (j == w.n_kv - 1) umma_commit(q_empty);  // last read of this item's Q
                     if (pg >= 0) issue_pv();
                     pg = g;
                     pst = st;
@@ -274,9 +278,9 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
         int n = 0;
         for (int64_t it = blockIdx.x; it < p.n_items; it += gridDim.x, ++n) {
             const Item w = decode(p, it);
-            const int qbuf = n & 1, ob = n % NOB;
+            const int ob = n % NOB;
             const uint32_t tO = tO0 + (uint32_t)ob * 128 + lane_base;
-            const uint8_t* qsm = smem + SM::q_off + qbuf * kTileBytes;
+            const uint8_t* qsm = smem + SM::q_off;
             const int grow = w.qtile * kTile + row;  // row within the segment
             const bool valid = grow < a.q_len;
             float c = 1.f;
@@ -292,7 +296,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
             const int last_valid = kTile - (kv_end > a.kv_len ? kv_end - a.kv_len : 0) - 64 * h;  // in my half
 
             if (a.check_finite) {
-                mbar_wait_sleep(&q_full[qbuf], (n >> 1) & 1);
+                mbar_wait_sleep(q_full, n & 1);
                 bool bad = false;
                 // each half checks one 64-column panel of the row
                 const uint4* q4 = reinterpret_cast<const uint4*>(qsm + h * kPanel + row * 128);
@@ -401,10 +405,11 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
 
             // -------------------------------------------------------- epilogue
             // full row sum from the two halves
-            float* lx = xch + 2 * 256;
-            lx[h * 128 + row] = l_run;
+            float* ex = xch + (g & 1) * 256;  // slot of the next tile: free after tile g-1's barrier
+            ex[h * 128 + row] = l_run;
             named_bar_sync(1, 256);
-            const float l_tot = lx[row] + lx[128 + row];
+            const float l_tot = ex[row] + ex[128 + row];
+            named_bar_sync(1, 256);  // trailing: the slot is reused below / by the next item
             mbar_wait_sleep(&o_full[ob], (n / NOB) & 1);
             tc_fence_after();
             const float inv_l = 1.f / l_tot;
@@ -429,6 +434,8 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
             } else {
                 float qo = 0.f;  // this half's part of <q_row, (P K)_row> (R-step entropy)
                 const int64_t obh = w.u / a.oHn, ohh = w.u % a.oHn;
+                const __nv_bfloat16* qrow = static_cast<const __nv_bfloat16*>(a.q_rows) + (w.u / a.qrHn) * a.qrB +
+                                            (w.u % a.qrHn) * a.qrH + (int64_t)w.seg * a.qrS + (int64_t)grow * a.qrR;
 #pragma unroll
                 for (int t = 0; t < NO; ++t) {
                     __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(t == 0 ? a.out0 : a.out1) + obh * a.oB[t] +
@@ -439,10 +446,12 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                         VMB_TMEM_LD32(tO + t * 128 + 64 * h + cc * 32, orr);
                         tmem_ld_wait();
                         if (t == 0 && a.cl_out) {
-                            const uint8_t* qp = qsm + h * kPanel;  // columns [64h, 64h+64)
+                            // the q row from global memory (L2): the Q smem buffer already
+                            // belongs to the next item
+                            const uint4* qp = reinterpret_cast<const uint4*>(qrow + 64 * h + cc * 32);
 #pragma unroll
                             for (int x = 0; x < 4; ++x) {
-                                const uint4 qv = *reinterpret_cast<const uint4*>(qp + sw128_offset(row, cc * 32 + 8 * x));
+                                const uint4 qv = valid ? __ldg(qp + x) : make_uint4(0, 0, 0, 0);
                                 const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
 #pragma unroll
                                 for (int e = 0; e < 4; ++e) {
@@ -467,10 +476,10 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                 }
                 if (a.cl_out) {
                     // combine the two halves of the entropy dot product
-                    float* qx = xch + 3 * 256;
-                    qx[h * 128 + row] = qo;
+                    ex[h * 128 + row] = qo;
                     named_bar_sync(1, 256);
-                    qo = qx[row] + qx[128 + row];
+                    qo = ex[row] + ex[128 + row];
+                    named_bar_sync(1, 256);
                 }
                 if (valid && h == 0) {
                     if (a.cl_out)
@@ -478,10 +487,9 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                     if (a.lse_out) a.lse_out[((int64_t)w.u * a.nseg + w.seg) * a.q_len + grow] = kLn2 * lse2;
                 }
             }
-            // O buffer and Q buffer of this item are free for the items two ahead
+            // this item's O buffer is free for the item NOB ahead
             tc_fence_before();
             mbar_arrive(&o_empty[ob]);
-            mbar_arrive(&q_empty[qbuf]);
         }
     }
 

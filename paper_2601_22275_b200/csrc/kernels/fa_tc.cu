@@ -24,6 +24,8 @@
 // (flash_entropy.hpp:25-51) but without per-tile rescaling.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "../internal.hpp"
 #include "sm100_ptx.cuh"
 
@@ -98,7 +100,12 @@ struct Smem {
     static constexpr uint32_t alloc = bytes + 1024;  // alignment slack
 };
 
-template <int NB, int NO>
+// MC: CTAs of adjacent query tiles form 2-CTA clusters; each K/V stage is loaded once per
+// cluster (CTA 0 fetches the K tile, CTA 1 the V tile -- or halves of the K tile when NB == 1)
+// and multicast into both CTAs, halving the L2 -> SMEM stream (at one CTA per SM the last
+// R-step needs ~11 TB/s of K|V tiles at full MMA rate, the TMA ceiling).  A stage is refilled
+// only when both CTAs' MMAs have released it (kv_empty counts 2 multicast commits).
+template <int NB, int NO, bool MC>
 __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constant__ Params p) {
     using SM = Smem<NB, NO>;
     constexpr int S = SM::S;
@@ -128,7 +135,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
         mbar_init(q_full, 1);
         for (int s = 0; s < S; ++s) {
             mbar_init(&kv_full[s], 1);
-            mbar_init(&kv_empty[s], 1);
+            mbar_init(&kv_empty[s], MC ? 2 : 1);
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&s_full[s], 1);
@@ -140,8 +147,10 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
     }
     if (warp == 1) tmem_alloc<512>(tmem_slot);
     tc_fence_before();
-    __syncthreads();
+    if (MC) cluster_sync();  // peers' barriers initialised before any multicast lands
+    else __syncthreads();
     tc_fence_after();
+    const uint32_t crank = MC ? cluster_ctarank() : 0;
     const uint32_t tmem = *tmem_slot;
     const uint32_t tS0 = tmem, tO = tmem + 256;
 
@@ -160,6 +169,20 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
                 if (j >= S) mbar_wait_sleep(&kv_empty[st], ((j / S) + 1) & 1);
                 uint8_t* skv = smem + SM::kv_off + st * NB * kTileBytes;
                 mbar_arrive_expect_tx(&kv_full[st], NB * kTileBytes);
+                if (MC) {
+                    // this CTA fetches one half of the stage (a whole tile when NB == 2, one
+                    // 64-column panel of the K tile when NB == 1) for both CTAs
+                    if (NB == 2) {
+                        const CUtensorMap* map = crank == 0 ? &a.tmK : &a.tmV;
+                        uint8_t* dst = skv + crank * kTileBytes;
+                        tma_load_5d_mc(dst, map, &kv_full[st], 0x3, 0, j * kTile, kseg, kh, kb);
+                        tma_load_5d_mc(dst + kPanelBytes, map, &kv_full[st], 0x3, 64, j * kTile, kseg, kh, kb);
+                    } else {
+                        tma_load_5d_mc(skv + crank * kPanelBytes, &a.tmK, &kv_full[st], 0x3, 64 * crank, j * kTile,
+                                       kseg, kh, kb);
+                    }
+                    continue;
+                }
                 tma_load_5d(skv, &a.tmK, &kv_full[st], 0, j * kTile, kseg, kh, kb);
                 tma_load_5d(skv + kPanelBytes, &a.tmK, &kv_full[st], 64, j * kTile, kseg, kh, kb);
                 if (NB == 2) {
@@ -214,7 +237,8 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
                             umma_ts(tO, tP + kk * 8, sdesc_sw128(vaddr + kk * 2048, kPanelBytes, 1024), idPV,
                                     (jp > 0 || kk > 0) ? 1u : 0u);
                     }
-                    umma_commit(&kv_empty[st]);
+                    if (MC) umma_commit_mc(&kv_empty[st], 0x3);  // release the stage in both CTAs
+                    else umma_commit(&kv_empty[st]);
                     umma_commit(pv_done);
                 }
             }
@@ -412,22 +436,36 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
     }
 
     tc_fence_before();
-    __syncthreads();
+    if (MC) cluster_sync();  // no CTA leaves while its peer may still multicast into it
+    else __syncthreads();
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc<512>(tmem);
     }
 }
 
-template <int NB, int NO>
+template <int NB, int NO, bool MC>
 void launch(const Params& p, int64_t U, cudaStream_t s) {
     using SM = Smem<NB, NO>;
-    auto kern = fa_tc_kernel<NB, NO>;
-    VMB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)SM::alloc));
-    dim3 grid((unsigned)((p.a.q_len + kTile - 1) / kTile), (unsigned)(U * p.a.nseg));
+    auto kern = fa_tc_kernel<NB, NO, MC>;
+    VMB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM::alloc));
+    unsigned qt = (unsigned)((p.a.q_len + kTile - 1) / kTile);
+    if (MC) qt = (qt + 1) & ~1u;  // whole clusters; a padding CTA computes zero rows, stores nothing
+    dim3 grid(qt, (unsigned)(U * p.a.nseg));
     ProfScope ps(NO == 2 ? kKRstepY : (NB == 1 ? kKRstep : kKAttn), s);
-    kern<<<grid, kThreads, SM::alloc, s>>>(p);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = SM::alloc;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = MC ? 2 : 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    VMB_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
     count_launch();
     check_launch("fa_tc");
 }
@@ -442,8 +480,20 @@ void tc_fa_launch(const TcFaArgs& a, int64_t U, cudaStream_t s) {
     Params p;
     p.a = a;
     p.n_kv_tiles = (a.kv_len + kTile - 1) / kTile;
-    if (a.nv == 2) launch<2, 2>(p, U, s);
-    else if (a.v_is_k) launch<1, 1>(p, U, s);
+    // 2-CTA multicast clusters only with VMB_FA_MC=1: measured slower on B200 (the two CTAs of
+    // a cluster advance in lock-step; the L2 -> SMEM stream was not the binding limit),
+    // profiles/r1_fa_variants.md
+    static const bool mc = [] {
+        const char* e = getenv("VMB_FA_MC");
+        return e && e[0] == '1';
+    }();
+    if (a.nv == 2) {
+        if (mc) launch<2, 2, true>(p, U, s);
+        else launch<2, 2, false>(p, U, s);
+    } else if (a.v_is_k) {
+        if (mc) launch<1, 1, true>(p, U, s);
+        else launch<1, 1, false>(p, U, s);
+    }
     else VMB_REQUIRE_DIM(false, "fa_tc serves the R half-steps only");
 }
 

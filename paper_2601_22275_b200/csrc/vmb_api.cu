@@ -151,8 +151,19 @@ int attn_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg) {
         default: return tc3_plan_splits(q_len, kv_len, n_useg, kTc2MaxSplit);
     }
 }
-Tc4Args to_tc4(const Tc2Args& a) {
+// query rows for fa4's entropy dot: row (u, s, r) at base + (u/Hn)*B + (u%Hn)*H + s*S + r*R
+struct QRows {
+    const void* base = nullptr;
+    int64_t B = 0, H = 0, S = 0, R = 0;
+    int32_t Hn = 1;
+};
+void set_qrows(Tc4Args& r, const QRows& q) {
+    r.q_rows = q.base;
+    r.qrB = q.B; r.qrH = q.H; r.qrS = q.S; r.qrR = q.R; r.qrHn = q.Hn;
+}
+Tc4Args to_tc4(const Tc2Args& a, const QRows& qv = QRows{}) {
     Tc4Args r{};
+    set_qrows(r, qv);
     r.tmQ = a.tmQ; r.tmK = a.tmK; r.tmV = a.tmV;
     r.nseg = a.nseg; r.q_len = a.q_len; r.kv_len = a.kv_len;
     r.qH = a.qH; r.kH = a.kH; r.oHn = a.oHn;
@@ -165,8 +176,9 @@ Tc4Args to_tc4(const Tc2Args& a) {
     r.part_o = a.part_o; r.part_lse = a.part_lse; r.max_split = a.max_split;
     return r;
 }
-Tc4Args to_tc4(const TcFaArgs& a) {
+Tc4Args to_tc4(const TcFaArgs& a, const QRows& qv) {
     Tc4Args r{};
+    set_qrows(r, qv);
     r.tmQ = a.tmQ; r.tmK = a.tmK; r.tmV = a.tmV;
     r.nseg = a.nseg; r.q_len = a.q_len; r.kv_len = a.kv_len;
     r.qH = a.qH; r.kH = a.kH; r.oHn = a.oHn;
@@ -179,10 +191,10 @@ Tc4Args to_tc4(const TcFaArgs& a) {
     return r;
 }
 // a.nv == 2: value operand V (attention); a.nv == 1: value = key (R half-step)
-void attn_launch(const Tc2Args& a, int64_t U, cudaStream_t s, bool rstep) {
+void attn_launch(const Tc2Args& a, int64_t U, cudaStream_t s, bool rstep, const QRows& qv = QRows{}) {
     switch (attn_impl(rstep)) {
         case 2: tc2_fa_launch(a, U, s); break;
-        case 4: tc4_fa_launch(to_tc4(a), U, s); break;
+        case 4: tc4_fa_launch(to_tc4(a, qv), U, s); break;
         case 1:  // original 1-CTA/SM kernel (R half-step only)
         default:
             if (rstep && attn_impl(true) == 1) {
@@ -427,9 +439,17 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
             fa.lse_out = nullptr;
             fa.status = ws.status;
             fa.check_finite = t == 0;
+            // query rows of this half-step (fa4's entropy dot reads them from global memory)
+            QRows qv;
+            if (t == 0) {
+                qv.base = q; qv.B = in.batch; qv.H = in.head; qv.S = bq * in.token; qv.R = in.token;
+                qv.Hn = (int32_t)std::max<int64_t>(s.H, 1);
+            } else {
+                qv.base = ws.aR; qv.B = m * bq * d; qv.H = 0; qv.S = bq * d; qv.R = d; qv.Hn = 1;
+            }
             if (last) {
                 // last R half-step with y = R V fused: O = P [K | V]
-                if (attn_impl(true) == 4) tc4_fa_launch(to_tc4(fa), U, st);
+                if (attn_impl(true) == 4) tc4_fa_launch(to_tc4(fa, qv), U, st);
                 else tc_fa_launch(fa, U, st);
             } else {
                 // R half-step without y: the 2-CTA/SM kernel (value operand = key tile)
@@ -454,7 +474,8 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
                 f2.status = ws.status;
                 f2.check_finite = fa.check_finite;
                 f2.max_split = 1;
-                attn_launch(f2, U, st, true);
+                if (attn_impl(true) == 4) f2.tmK = f2.tmV = mK;  // fa4: 128-key tiles
+                attn_launch(f2, U, st, true, qv);
             }
 
             TcLstepArgs ls{};
@@ -836,7 +857,9 @@ vmb_status vmb_rstep(int64_t units, int64_t m, int64_t b, int64_t d, vmb_dtype d
             int32_t* dummy = nullptr;
             VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dummy), sizeof(int32_t), st));
             f2.status = dummy;
-            attn_launch(f2, units, st, true);
+            QRows qv;
+            qv.base = aR; qv.B = m * b * d; qv.H = 0; qv.S = b * d; qv.R = d; qv.Hn = 1;
+            attn_launch(f2, units, st, true, qv);
             VMB_CHECK_CUDA(cudaFreeAsync(dummy, st));
             return;
         }
