@@ -192,6 +192,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-chunk", type=int, default=2, help="heads per H2D/compute/D2H chunk in the e2e path")
     ap.add_argument("--shard", default="heads", choices=["heads", "seq"],
                     help="multi-GPU split: heads (no inter-GPU traffic) or seq (spatial slabs, NCCL K/V all-gather)")
     args = ap.parse_args()
@@ -341,14 +342,10 @@ def main():
         hv = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
         ho = torch.empty(o.shape, dtype=o.dtype, pin_memory=True)
         hq.copy_(q); hk.copy_(k); hv.copy_(v)
-        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
 
         def e2e_step():
-            dq.copy_(hq, non_blocking=True)
-            dk.copy_(hk, non_blocking=True)
-            dv.copy_(hv, non_blocking=True)
-            vm.vmonarch_attention(dq, dk, dv, grid, cfg, out=o, check=False)
-            ho.copy_(o, non_blocking=True)
+            # public host-buffer API: chunks of heads stream H2D -> forward -> D2H on 3 streams
+            vm.vmonarch_attention_host(hq, hk, hv, grid, cfg, out=ho, chunk_units=args.e2e_chunk)
 
         e2e_step()
         torch.cuda.synchronize()
@@ -362,7 +359,8 @@ def main():
         e2e = {"value": round(e2e_ms, 3), "unit": "ms/call",
                "h2d_bytes_per_step": 3 * q.numel() * q.element_size(),
                "d2h_bytes_per_step": o.numel() * o.element_size(),
-               "path": "pinned host Q/K/V -> HBM, vmonarch_attention (libvmb C ABI), O -> pinned host"}
+               "path": (f"vmonarch_attention_host: pinned host Q/K/V -> HBM -> libvmb forward -> pinned host O, "
+                        f"{args.e2e_chunk} heads per chunk pipelined over 3 CUDA streams")}
 
     # ---- dense FlashAttention-style bf16 baseline on the same GPU (same heads)
     dense = None

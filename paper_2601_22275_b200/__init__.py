@@ -30,7 +30,7 @@ __all__ = [
     "TokenGrid", "VMonarchConfig", "CostReport", "DimensionError", "DomainError", "StateError",
     "vmonarch_attention", "r_update", "l_update", "flash_entropy_fwd", "dense_forward",
     "factorize", "flops_estimate", "make_perm", "preset_grid", "export_factors", "lib",
-    "kernel_launch_count", "LIB_PATH", "vmonarch_attention_slab", "seq_assemble",
+    "kernel_launch_count", "LIB_PATH", "vmonarch_attention_slab", "seq_assemble", "vmonarch_attention_host",
 ]
 
 LIB_PATH = os.environ.get("VMB_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libvmb.so")
@@ -312,6 +312,79 @@ def vmonarch_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, grid: 
                            _ptr(R), st))
         factors_out.clear()
         factors_out.extend((L[u], R[u]) for u in range(U))
+    return out
+
+
+# ----------------------------------------------------------------------------- host-buffer pipeline
+class _HostPipeline:
+    """Device buffers + streams reused across vmonarch_attention_host calls of one shape."""
+
+    def __init__(self, shape, dtype, device, chunk, nbuf):
+        self.key = (shape, dtype, device, chunk, nbuf)
+        self.bufs = [tuple(torch.empty((chunk,) + tuple(shape[1:]), dtype=dtype, device=device) for _ in range(4))
+                     for _ in range(nbuf)]
+        self.h2d = torch.cuda.Stream(device)
+        self.comp = torch.cuda.Stream(device)
+        self.d2h = torch.cuda.Stream(device)
+
+
+_PIPE: dict = {}
+
+
+def vmonarch_attention_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, grid: TokenGrid,
+                            cfg: VMonarchConfig = VMonarchConfig(), out: Optional[torch.Tensor] = None,
+                            chunk_units: int = 8, device=None) -> torch.Tensor:
+    """video.hpp:84-150 for HOST tensors (units, N, d): batch*head units are independent
+    (video.hpp:131-148), so chunks of units stream through the device -- the H2D copy of chunk
+    c+1, the forward of chunk c and the D2H copy of chunk c-1 run on three CUDA streams.
+    Inputs should be pinned for the copies to overlap.  Returns the host output."""
+    if q.is_cuda or k.is_cuda or v.is_cuda:
+        raise DimensionError("dimension error: vmonarch_attention_host takes host tensors")
+    device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    U = q.shape[0]
+    if U != grid.units() or q.dim() != 3:
+        raise DimensionError(f"dimension error: expected (units={grid.units()}, N, d) host tensors")
+    if out is None:
+        out = torch.empty(q.shape, dtype=q.dtype, pin_memory=True)
+    chunk = max(1, min(chunk_units, U))
+    nbuf = 2
+    key = (tuple(q.shape), q.dtype, device, chunk, nbuf)
+    pipe = _PIPE.get(key)
+    if pipe is None:
+        _PIPE.clear()
+        pipe = _PIPE[key] = _HostPipeline(tuple(q.shape), q.dtype, device, chunk, nbuf)
+    cur = torch.cuda.current_stream(device)
+    h2d, comp, d2h = pipe.h2d, pipe.comp, pipe.d2h
+    h2d.wait_stream(cur)
+    ev_in = [None] * nbuf      # chunk's inputs resident
+    ev_done = [None] * nbuf    # chunk's output computed
+    ev_free = [None] * nbuf    # buffer set drained to host
+    starts = list(range(0, U, chunk))
+    for c, a in enumerate(starts):
+        b = min(a + chunk, U)
+        n = b - a
+        slot = c % nbuf
+        dq, dk, dv, do = pipe.bufs[slot]
+        with torch.cuda.stream(h2d):
+            if ev_free[slot] is not None:
+                h2d.wait_event(ev_free[slot])
+            dq[:n].copy_(q[a:b], non_blocking=True)
+            dk[:n].copy_(k[a:b], non_blocking=True)
+            dv[:n].copy_(v[a:b], non_blocking=True)
+            ev_in[slot] = torch.cuda.Event()
+            ev_in[slot].record(h2d)
+        with torch.cuda.stream(comp):
+            comp.wait_event(ev_in[slot])
+            g = TokenGrid(grid.t_frames, grid.h, grid.w, grid.head_dim, n, 1)
+            vmonarch_attention(dq[:n], dk[:n], dv[:n], g, cfg, out=do[:n], check=False)
+            ev_done[slot] = torch.cuda.Event()
+            ev_done[slot].record(comp)
+        with torch.cuda.stream(d2h):
+            d2h.wait_event(ev_done[slot])
+            out[a:b].copy_(do[:n], non_blocking=True)
+            ev_free[slot] = torch.cuda.Event()
+            ev_free[slot].record(d2h)
+    cur.wait_stream(d2h)
     return out
 
 
