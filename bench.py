@@ -322,7 +322,8 @@ def main():
         traffic = None
         try:
             with open(os.path.join(HERE, "profiles", "ncu_traffic.json")) as f:
-                traffic = json.load(f).get(dom)
+                t_ = json.load(f).get(dom)
+                traffic = t_.get("bytes") if isinstance(t_, dict) else t_
         except Exception:
             pass
         roof = {"kernel": dom, "bound": bound, "achieved": round(ach, 1), "peak": peak, "unit": unit,

@@ -22,10 +22,11 @@ OUT = os.path.join(HERE, "gpurun_out")
 PROF = os.path.join(HERE, "profiles")
 
 # kernel-name fragment -> bench.py kernel key
-KEYS = [("fa_tc_kernel<1, 1>", "rstep"), ("fa_tc_kernel<2, 2>", "rstep_y"), ("fa_tc_kernel<2, 1>", "attn_recompute"),
-        ("fa2_kernel<1>", "rstep"), ("fa2_kernel<2>", "attn_recompute"), ("fa2_kernel", "attn"),
-        ("lstep_tc_kernel<0>", "lstep"), ("lstep_tc_kernel<1>", "lstep_apply"),
-        ("lstep2_kernel<0>", "lstep"), ("lstep2_kernel<1>", "lstep_apply"), ("combine", "combine")]
+KEYS = [("fa_tc_kernel<2, 2", "rstep_y"), ("fa_tc_kernel<1, 1", "rstep"), ("fa2_kernel<1>", "rstep"),
+        ("fa2_kernel<2>", "attn_recompute"), ("fa3_kernel<2>", "attn_recompute"), ("fa3_kernel<1>", "rstep"),
+        ("fa4_kernel<1, 1>", "rstep"), ("fa4_kernel<2, 2>", "rstep_y"), ("fa4_kernel<2, 1>", "attn_recompute"),
+        ("lstep_tc_kernel<0", "lstep"), ("lstep_tc_kernel<1", "lstep_apply"), ("fa2_combine", "combine"),
+        ("seq_assemble", "seq_assemble")]
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
            "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
