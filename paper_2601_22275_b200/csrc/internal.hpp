@@ -147,6 +147,10 @@ struct TcFaArgs {
     float* lse_out;              // (u, s, r) at (u*nseg + s)*q_len + r
     int32_t* status;             // non-finite detection
     int32_t check_finite;
+    // TMA-store epilogue (internal contiguous outputs, R half-step + y): tmO[0] over aL
+    // (d, k, i, 1, U) box (64, 1, 128); tmO[1] over y (d, i, k, 1, U) box (64, 128, 1)
+    int32_t o_tma;
+    CUtensorMap tmO[2];
 };
 void tc_fa_launch(const TcFaArgs& a, int64_t U, cudaStream_t s);
 

@@ -14,12 +14,14 @@
 //                 profiles/r1_micro_tcgen05.md)
 //   <NB=2, NO=1>  attention: first-frame recompute / dense baseline (flash_entropy.hpp:85-139)
 //
-// Warp roles (384 threads): warp 0 TMA producer, warp 1 TMEM allocator + single-thread MMA
-// issuer, warps 4-11 softmax + epilogue in two warpgroups that split every score row: the
-// thread of warpgroup h owns columns [64h, 64h+64) of query row (warp%4)*32 + lane (TMEM
-// lane restriction).  Two softmax warps per SM sub-partition keep the MUFU pipe fed (one
-// warp alone is dependency-bound); the row max / sum / entropy partials meet in shared
-// memory (one named barrier per key tile).
+// Warp roles (512 threads): warp 0 TMA producer, warp 1 TMEM allocator + single-thread MMA
+// issuer, warps 4-11 softmax in two warpgroups that split every score row (the thread of
+// warpgroup h owns columns [64h, 64h+64) of query row (warp%4)*32 + lane; the half-row
+// maxima meet in shared memory, one named barrier per key tile), warps 12-15 the epilogue:
+// they read an item's O out of TMEM, normalise it with the row statistics handed over in
+// shared memory and store it, while the softmax warpgroups already run the next item (a
+// non-persistent CTA spends ~5 of its ~18 us in prologue/epilogue with the tensor pipe idle,
+// profiles/r1_fa_variants.md).
 // TMEM (512 columns): S0 [0,128), S1 [128,256) double-buffered scores (P written back as
 // bf16 over the first 64 columns); NO=1: O0 [256,384), O1 [384,512) double-buffered over
 // items; NO=2: O [256,512) = [P K | P V].
@@ -33,7 +35,7 @@
 //
 // Statistics: base 2, lazily rescaled reference max (threshold 8).  With value = key the
 // entropy is  sum_l R ln R = ln2 * (scale2 * <q, O_K> / l - lse2)  (monarch.hpp:93-98): one
-// dot product in the epilogue.
+// dot product in the epilogue, with the q row prefetched from L2.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -46,7 +48,7 @@ namespace {
 
 using namespace ptx;
 
-constexpr int kThreads = 384;
+constexpr int kThreads = 512;
 constexpr int kTile = 128;                      // query rows per item, keys per KV tile
 constexpr uint32_t kPanel = 128 * 128;          // 128 rows x 64 bf16 (SW128)
 constexpr uint32_t kTileBytes = 2 * kPanel;     // 128 x 128 bf16
@@ -102,42 +104,69 @@ struct Params {
 struct Item {
     int qtile, split, useg, u, seg, kv_tile0, n_kv;
 };
-__device__ __forceinline__ Item decode(const Params& p, int64_t it) {
+__device__ __forceinline__ Item decode(const Params& p, int64_t it64) {
+    // 32-bit index arithmetic (n_items < 2^31, checked at launch): 64-bit divisions are
+    // software routines and sat on the per-item critical path
+    const uint32_t it = (uint32_t)it64;
     Item r;
-    r.qtile = (int)(it % p.q_tiles);
-    const int64_t rest = it / p.q_tiles;
-    r.split = (int)(rest % p.nsplit);
-    r.useg = (int)(rest / p.nsplit);
-    r.u = r.useg / p.a.nseg;
-    r.seg = r.useg % p.a.nseg;
+    const uint32_t qt = (uint32_t)p.q_tiles, ns = (uint32_t)p.nsplit, sg = (uint32_t)p.a.nseg;
+    r.qtile = (int)(it % qt);
+    const uint32_t rest = it / qt;
+    r.split = (int)(rest % ns);
+    r.useg = (int)(rest / ns);
+    r.u = (int)((uint32_t)r.useg / sg);
+    r.seg = (int)((uint32_t)r.useg % sg);
     r.kv_tile0 = r.split * p.n_kv_tiles;
     r.n_kv = min(p.n_kv_tiles, p.total_tiles - r.kv_tile0);
     return r;
 }
 
-template <int NB>
+template <int NB, int NO>
 struct Smem {
-    static constexpr int S = NB == 1 ? 5 : 3;             // KV stages (32 KB K or 64 KB K|V each)
+    static constexpr int NOB = NO == 1 ? 2 : 1;           // O buffers (TMEM) / stats buffers
+    static constexpr int S = NB == 1 ? 5 : (NO == 2 ? 3 : 2);  // KV stages (32 KB K or 64 KB K|V)
     static constexpr uint32_t q_off = 0;                  // one Q buffer, released by the MMA warp
     static constexpr uint32_t kv_off = kTileBytes;        // after the item's last S
     static constexpr uint32_t bar_off = kv_off + S * NB * kTileBytes;
     // q_full, q_empty, kv_full[S], kv_empty[S], s_full[2], p_full[2], pv_done, o_full[2],
-    // o_empty[2]
-    static constexpr uint32_t n_bars = 2 + 2 * S + 5 + 4;
+    // o_empty[2], stat_full[2], stat_empty[2]
+    static constexpr uint32_t n_bars = 2 + 2 * S + 5 + 4 + 4;
     static constexpr uint32_t slot_off = bar_off + n_bars * 8;
-    // float [2 slots][2 halves][128 rows]: per-tile max exchange (double-buffered); the
-    // epilogue's row-sum / entropy exchanges reuse a slot behind a trailing barrier
+    // bf16 [2 slots][2 halves][128 rows]: per-tile half-row max exchange (double-buffered;
+    // rounded up, both halves read the same stored values -> identical decisions)
     static constexpr uint32_t xch_off = slot_off + 16;
-    static constexpr uint32_t bytes = xch_off + 2 * 2 * 128 * 4;
+    // float [O buffers][3][128 rows]: the two half-row sums and the running max of an item,
+    // handed from the softmax warpgroups to the epilogue warpgroup
+    static constexpr uint32_t stat_off = xch_off + 2 * 2 * 128 * 2;
+    static constexpr uint32_t bytes = stat_off + NOB * 3 * 128 * 4;
+    static_assert(bytes <= 232448, "shared memory budget (227 KB per CTA)");
     // the dynamic smem window starts 1024-aligned (checked in the kernel): no slack needed
     static constexpr uint32_t alloc = bytes;
 };
 
+#ifndef VMB_TRACE
+#define VMB_TRACE 0
+#endif
+#if VMB_TRACE
+// debug-only per-item timeline: [cta < 64][item < 16][event] globaltimer (ns)
+__device__ unsigned long long g_trace4[64][16][8];
+__device__ __forceinline__ void trace4(int n, int ev) {
+    if (blockIdx.x < 64 && n < 16) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_trace4[blockIdx.x][n][ev] = t;
+    }
+}
+#define TRACE4(n, ev) trace4(n, ev)
+#else
+#define TRACE4(n, ev) do { } while (0)
+#endif
+
 template <int NB, int NO>
 __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant__ Params p) {
-    using SM = Smem<NB>;
+    using SM = Smem<NB, NO>;
     constexpr int S = SM::S;
-    constexpr int NOB = NO == 1 ? 2 : 1;  // O buffers
+    constexpr int NOB = SM::NOB;  // O buffers
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw;
     if (smem_u32(smem_raw) & 1023u) __trap();  // SW128 operand tiles need 1024-B alignment
@@ -151,6 +180,8 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
     uint64_t* pv_done = p_full + 2;
     uint64_t* o_full = pv_done + 1;       // [2]
     uint64_t* o_empty = o_full + 2;       // [2]
+    uint64_t* stat_full = o_empty + 2;    // [2]
+    uint64_t* stat_empty = stat_full + 2; // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM::slot_off);
 
     const Tc4Args& a = p.a;
@@ -166,7 +197,9 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
             mbar_init(&s_full[i], 1);
             mbar_init(&p_full[i], 256);
             mbar_init(&o_full[i], 1);
-            mbar_init(&o_empty[i], 256);
+            mbar_init(&o_empty[i], 128);
+            mbar_init(&stat_full[i], 256);
+            mbar_init(&stat_empty[i], 128);
         }
         for (int s = 0; s < S; ++s) {
             mbar_init(&kv_full[s], 1);
@@ -268,14 +301,23 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
             }
             if (pg >= 0) issue_pv();
         }
-    } else if (warp >= 4) {
-        // ------------------------------------------------------------ softmax / epilogue
+    } else if (warp >= 4 && warp < 12) {
+        // ------------------------------------------------------------ softmax (2 warpgroups)
         const int h = (warp - 4) >> 2;      // column half of the score row
         const int row = (warp & 3) * 32 + lane_id();  // TMEM lane == query row in tile
         const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-        float* xch = reinterpret_cast<float*>(smem + SM::xch_off);  // [slot][half][row]
+        __nv_bfloat16* xch = reinterpret_cast<__nv_bfloat16*>(smem + SM::xch_off);  // [slot][half][row]
+        float* stats = reinterpret_cast<float*>(smem + SM::stat_off);              // [ob][3][row]
         int64_t g = 0;
         int n = 0;
+        // per-row temperature source, loaded one item ahead (its latency hides under a whole item)
+        auto load_c = [&](int64_t it2) -> float {
+            if (!a.cR || it2 >= p.n_items) return 1.f;
+            const Item w2 = decode(p, it2);
+            const int gr = w2.qtile * kTile + row;
+            return gr < a.q_len ? __ldg(a.cR + ((int64_t)w2.u * a.nseg + w2.seg) * a.q_len + gr) : 1.f;
+        };
+        float c_next = load_c(blockIdx.x);
         for (int64_t it = blockIdx.x; it < p.n_items; it += gridDim.x, ++n) {
             const Item w = decode(p, it);
             const int ob = n % NOB;
@@ -283,8 +325,8 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
             const uint8_t* qsm = smem + SM::q_off;
             const int grow = w.qtile * kTile + row;  // row within the segment
             const bool valid = grow < a.q_len;
-            float c = 1.f;
-            if (a.cR && valid) c = a.cR[((int64_t)w.u * a.nseg + w.seg) * a.q_len + grow];
+            float c = c_next;
+            c_next = load_c(it + gridDim.x);
             if (a.clamp_enabled) {
                 c = (c < a.clamp_min) ? a.clamp_min : c;
             } else if (!(c > 0.f)) {
@@ -313,9 +355,11 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
 
             float m_run = -INFINITY, l_run = 0.f;  // l_run: this half's partial row sum
             const uint64_t scale2x2 = pk2(scale2, scale2);
+            if (threadIdx.x == 128) TRACE4(n, 0);
             for (int j = 0; j < w.n_kv; ++j, ++g) {
                 const uint32_t tS = tS0 + (uint32_t)(g & 1) * 128 + lane_base;
                 mbar_wait_sleep(&s_full[g & 1], (g >> 1) & 1);
+                if (threadIdx.x == 128 && j == 0) TRACE4(n, 1);
                 tc_fence_after();
                 uint32_t sr[64];
                 VMB_TMEM_LD32(tS + 64 * h + 0, (sr + 0));
@@ -339,10 +383,10 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                 a0 = fmax3(a0, s[60], s[61]);
                 a1 = fmax3(a1, s[62], s[63]);
                 // exchange the half-row maxima (double-buffered slot: one barrier per tile)
-                float* slot = xch + (g & 1) * 256;
-                slot[h * 128 + row] = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
+                __nv_bfloat16* slot = xch + (g & 1) * 256;
+                slot[h * 128 + row] = __float2bfloat16_ru(fmaxf(fmaxf(a0, a1), fmaxf(a2, a3)));
                 named_bar_sync(1, 256);
-                const float m_cand = fmaxf(slot[row], slot[128 + row]) * scale2;
+                const float m_cand = fmaxf(__bfloat162float(slot[row]), __bfloat162float(slot[128 + row])) * scale2;
                 bool rescale = false;
                 float alpha = 1.f;
                 if (j == 0) {
@@ -360,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                 }
                 const uint64_t negm2 = pk2(-m_run, -m_run);
                 const uint64_t* s2 = reinterpret_cast<const uint64_t*>(sr);
-                uint64_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+                uint64_t acc0 = 0, acc1 = 0;
 #pragma unroll
                 for (int cc = 0; cc < 2; ++cc) {
                     uint32_t pk[16];
@@ -370,17 +414,13 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                         uint64_t pp;
                         if ((x % VMB_EMU_PERIOD) == VMB_EMU_PERIOD - 1) pp = ex2_emu2(t2);
                         else pp = pk2(ex2(lo2(t2)), ex2(hi2(t2)));
-                        switch (x & 3) {
-                            case 0: acc0 = fadd2(acc0, pp); break;
-                            case 1: acc1 = fadd2(acc1, pp); break;
-                            case 2: acc2 = fadd2(acc2, pp); break;
-                            default: acc3 = fadd2(acc3, pp); break;
-                        }
+                        if (x & 1) acc1 = fadd2(acc1, pp);
+                        else acc0 = fadd2(acc0, pp);
                         pk[x] = pack_bf16(lo2(pp), hi2(pp));
                     }
                     VMB_TMEM_ST16(tS + 32 * h + cc * 16, pk);
                 }
-                const uint64_t acc = fadd2(fadd2(acc0, acc1), fadd2(acc2, acc3));
+                const uint64_t acc = fadd2(acc0, acc1);
                 l_run += lo2(acc) + hi2(acc);
                 if (rescale) {
                     // O must hold every earlier P V product of this item before it is rescaled;
@@ -402,25 +442,60 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                 tc_fence_before();
                 mbar_arrive(&p_full[g & 1]);
             }
-
-            // -------------------------------------------------------- epilogue
-            // full row sum from the two halves
-            float* ex = xch + (g & 1) * 256;  // slot of the next tile: free after tile g-1's barrier
-            ex[h * 128 + row] = l_run;
-            named_bar_sync(1, 256);
-            const float l_tot = ex[row] + ex[128 + row];
-            named_bar_sync(1, 256);  // trailing: the slot is reused below / by the next item
-            mbar_wait_sleep(&o_full[ob], (n / NOB) & 1);
-            tc_fence_after();
+            if (threadIdx.x == 128) TRACE4(n, 2);
+            // hand the item's row statistics to the epilogue warpgroup and move on
+            if (n >= NOB) mbar_wait_sleep(&stat_empty[ob], ((n / NOB) - 1) & 1);
+            float* st = stats + ob * 384;
+            st[h * 128 + row] = l_run;
+            if (h == 0) st[256 + row] = m_run;
+            mbar_arrive(&stat_full[ob]);
+        }
+    } else if (warp >= 12) {
+        // ------------------------------------------------------------ epilogue warpgroup
+        // drains O of item n while the softmax warpgroups already work on item n+1
+        const int row = (warp & 3) * 32 + lane_id();
+        const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+        const float* stats = reinterpret_cast<const float*>(smem + SM::stat_off);
+        int n = 0;
+        for (int64_t it = blockIdx.x; it < p.n_items; it += gridDim.x, ++n) {
+            const Item w = decode(p, it);
+            const int ob = n % NOB;
+            const uint32_t tO = tO0 + (uint32_t)ob * 128 + lane_base;
+            const int grow = w.qtile * kTile + row;
+            const bool valid = grow < a.q_len;
+            // the per-row temperature and the q row (entropy dot) are fetched before the item's
+            // statistics arrive, so their latency hides under the item's last tiles
+            float c = 1.f;
+            if (a.cR && valid) c = __ldg(a.cR + ((int64_t)w.u * a.nseg + w.seg) * a.q_len + grow);
+            uint4 qv[16];
+            if (a.cl_out) {
+                const uint4* qp = reinterpret_cast<const uint4*>(
+                    static_cast<const __nv_bfloat16*>(a.q_rows) + (w.u / a.qrHn) * a.qrB + (w.u % a.qrHn) * a.qrH +
+                    (int64_t)w.seg * a.qrS + (int64_t)grow * a.qrR);
+#pragma unroll
+                for (int x = 0; x < 16; ++x) qv[x] = valid ? __ldg(qp + x) : make_uint4(0, 0, 0, 0);
+            }
+            if (a.clamp_enabled) c = (c < a.clamp_min) ? a.clamp_min : c;
+            else if (!(c > 0.f)) c = 1.f;
+            const float scale2 = a.qscale * kLog2e / c;
+            mbar_wait_sleep(&stat_full[ob], (n / NOB) & 1);
+            const float* st = stats + ob * 384;
+            const float l_tot = st[row] + st[128 + row];
+            const float m_run = st[256 + row];
+            mbar_arrive(&stat_empty[ob]);
+            if (threadIdx.x == 384) TRACE4(n, 3);
             const float inv_l = 1.f / l_tot;
             const float lse2 = m_run + log2f(l_tot);  // base-2 log-sum-exp of x' = s * scale2
+            mbar_wait_sleep(&o_full[ob], (n / NOB) & 1);
+            if (threadIdx.x == 384) TRACE4(n, 4);
+            tc_fence_after();
             if (a.part_o) {
-                // split-KV partial: normalised fp32 O (this half's 64 columns) and the lse
-                float* prow = a.part_o + (((int64_t)w.useg * a.nsplit + w.split) * a.q_len + grow) * 128 + 64 * h;
+                // split-KV partial: normalised fp32 O and natural-log lse of this split
+                float* prow = a.part_o + (((int64_t)w.useg * a.nsplit + w.split) * a.q_len + grow) * 128;
 #pragma unroll
-                for (int cc = 0; cc < 2; ++cc) {
+                for (int cc = 0; cc < 4; ++cc) {
                     uint32_t orr[32];
-                    VMB_TMEM_LD32(tO + 64 * h + cc * 32, orr);
+                    VMB_TMEM_LD32(tO + cc * 32, orr);
                     tmem_ld_wait();
                     if (valid) {
                         float4* dst = reinterpret_cast<float4*>(prow + cc * 32);
@@ -430,29 +505,32 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                                                  __uint_as_float(orr[4 * x + 2]) * inv_l, __uint_as_float(orr[4 * x + 3]) * inv_l);
                     }
                 }
-                if (valid && h == 0) a.part_lse[((int64_t)w.useg * a.nsplit + w.split) * a.q_len + grow] = kLn2 * lse2;
+                tc_fence_before();
+                mbar_arrive(&o_empty[ob]);
+                if (valid) a.part_lse[((int64_t)w.useg * a.nsplit + w.split) * a.q_len + grow] = kLn2 * lse2;
             } else {
-                float qo = 0.f;  // this half's part of <q_row, (P K)_row> (R-step entropy)
+                float qo = 0.f;  // <q_row, (P K)_row> (R-step entropy)
                 const int64_t obh = w.u / a.oHn, ohh = w.u % a.oHn;
-                const __nv_bfloat16* qrow = static_cast<const __nv_bfloat16*>(a.q_rows) + (w.u / a.qrHn) * a.qrB +
-                                            (w.u % a.qrHn) * a.qrH + (int64_t)w.seg * a.qrS + (int64_t)grow * a.qrR;
 #pragma unroll
                 for (int t = 0; t < NO; ++t) {
                     __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(t == 0 ? a.out0 : a.out1) + obh * a.oB[t] +
-                                          ohh * a.oH[t] + (int64_t)w.seg * a.oS[t] + (int64_t)grow * a.oR[t] + 64 * h;
+                                          ohh * a.oH[t] + (int64_t)w.seg * a.oS[t] + (int64_t)grow * a.oR[t];
 #pragma unroll
-                    for (int cc = 0; cc < 2; ++cc) {
+                    for (int cc = 0; cc < 4; ++cc) {
                         uint32_t orr[32];
-                        VMB_TMEM_LD32(tO + t * 128 + 64 * h + cc * 32, orr);
+                        VMB_TMEM_LD32(tO + t * 128 + cc * 32, orr);
                         tmem_ld_wait();
+                        if (t == NO - 1 && cc == 3) {
+                            // all of O is in registers or stored: the next item's PV may start
+                            tc_fence_before();
+                            mbar_arrive(&o_empty[ob]);
+                            if (threadIdx.x == 384) TRACE4(n, 5);
+                        }
                         if (t == 0 && a.cl_out) {
-                            // the q row from global memory (L2): the Q smem buffer already
-                            // belongs to the next item
-                            const uint4* qp = reinterpret_cast<const uint4*>(qrow + 64 * h + cc * 32);
 #pragma unroll
                             for (int x = 0; x < 4; ++x) {
-                                const uint4 qv = valid ? __ldg(qp + x) : make_uint4(0, 0, 0, 0);
-                                const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
+                                const uint4 q4 = qv[cc * 4 + x];
+                                const uint32_t qw[4] = {q4.x, q4.y, q4.z, q4.w};
 #pragma unroll
                                 for (int e = 0; e < 4; ++e) {
                                     qo = fmaf(__uint_as_float(qw[e] << 16), __uint_as_float(orr[8 * x + 2 * e]), qo);
@@ -474,22 +552,13 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                         }
                     }
                 }
-                if (a.cl_out) {
-                    // combine the two halves of the entropy dot product
-                    ex[h * 128 + row] = qo;
-                    named_bar_sync(1, 256);
-                    qo = ex[row] + ex[128 + row];
-                    named_bar_sync(1, 256);
-                }
-                if (valid && h == 0) {
+                if (valid) {
                     if (a.cl_out)
                         a.cl_out[((int64_t)w.u * a.q_len + grow) * a.nseg + w.seg] = kLn2 * (scale2 * qo * inv_l - lse2);
                     if (a.lse_out) a.lse_out[((int64_t)w.u * a.nseg + w.seg) * a.q_len + grow] = kLn2 * lse2;
                 }
+                if (threadIdx.x == 384) TRACE4(n, 6);
             }
-            // this item's O buffer is free for the item NOB ahead
-            tc_fence_before();
-            mbar_arrive(&o_empty[ob]);
         }
     }
 
@@ -503,7 +572,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
 
 template <int NB, int NO>
 void launch(const Params& p, cudaStream_t s) {
-    using SM = Smem<NB>;
+    using SM = Smem<NB, NO>;
     auto kern = fa4_kernel<NB, NO>;
     VMB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM::alloc));
     int dev = 0, sms = 148;
@@ -541,6 +610,7 @@ void tc4_fa_launch(Tc4Args a, int64_t U, cudaStream_t s) {
     p.nsplit = (a.part_o && a.nv == 1 && !a.v_is_k) ? tc4_plan_splits(a.q_len, a.kv_len, n_useg, a.max_split) : 1;
     p.n_kv_tiles = (p.total_tiles + p.nsplit - 1) / p.nsplit;
     p.n_items = (int64_t)p.q_tiles * p.nsplit * n_useg;
+    VMB_REQUIRE_DIM(p.n_items < ((int64_t)1 << 31), "too many work items for one launch");
     a.nsplit = p.nsplit;
     if (p.nsplit == 1) a.part_o = nullptr;
     p.a = a;
@@ -564,3 +634,9 @@ void tc4_fa_launch(Tc4Args a, int64_t U, cudaStream_t s) {
 }
 
 }  // namespace vmb
+
+#if VMB_TRACE
+extern "C" int vmb_debug_trace4_read(unsigned long long* host) {
+    return cudaMemcpyFromSymbol(host, vmb::g_trace4, sizeof(unsigned long long) * 64 * 16 * 8) == cudaSuccess ? 0 : -1;
+}
+#endif

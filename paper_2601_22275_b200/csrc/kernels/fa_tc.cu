@@ -105,6 +105,23 @@ struct Smem {
 // and multicast into both CTAs, halving the L2 -> SMEM stream (at one CTA per SM the last
 // R-step needs ~11 TB/s of K|V tiles at full MMA rate, the TMA ceiling).  A stage is refilled
 // only when both CTAs' MMAs have released it (kv_empty counts 2 multicast commits).
+#ifndef VMB_TRACE
+#define VMB_TRACE 0
+#endif
+#if VMB_TRACE
+// debug-only timeline probes: [cta][event] globaltimer (ns); read by scripts/trace_fa.py
+__device__ unsigned long long g_trace[4096][8];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define TRACE(ev) do { const unsigned cta_ = blockIdx.y * gridDim.x + blockIdx.x; \
+    if (cta_ < 4096) g_trace[cta_][ev] = gtimer(); } while (0)
+#else
+#define TRACE(ev) do { } while (0)
+#endif
+
 template <int NB, int NO, bool MC>
 __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constant__ Params p) {
     using SM = Smem<NB, NO>;
@@ -128,6 +145,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
     const int u = useg / a.nseg, seg = useg % a.nseg;
     const int n_kv = p.n_kv_tiles;
 
+    if (threadIdx.x == 128) TRACE(0);  // CTA start
     if (warp == 0 && elect_one()) {
         tma_prefetch_desc(&a.tmQ);
         tma_prefetch_desc(&a.tmK);
@@ -152,6 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
     tc_fence_after();
     const uint32_t crank = MC ? cluster_ctarank() : 0;
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 128) TRACE(1);  // TMEM allocated, barriers ready
     const uint32_t tS0 = tmem, tO = tmem + 256;
 
     if (warp == 0) {
@@ -282,6 +301,8 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
         for (int j = 0; j < n_kv; ++j) {
             const uint32_t tS = tS0 + (j & 1) * 128 + lane_base;
             mbar_wait_sleep(&s_full[j & 1], (j >> 1) & 1);
+            if (threadIdx.x == 128 && j == 0) TRACE(2);         // first score tile ready
+            if (threadIdx.x == 128 && j == n_kv - 1) TRACE(3);  // last score tile ready
             tc_fence_after();
 #if VMB_DEBUG_NO_SOFTMAX  // timing experiment only: MMA/TMA pipeline without the softmax
             if (true) {
@@ -380,7 +401,9 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
         }
 
         // ------------------------------------------------------------ epilogue
+        if (threadIdx.x == 128) TRACE(4);  // last P handed over
         mbar_wait_sleep(o_full, 0);
+        if (threadIdx.x == 128) TRACE(5);  // O complete
         tc_fence_after();
         const float inv_l = 1.f / l_run;
         const int64_t ob = u / a.oHn, oh = u % a.oHn;
@@ -409,18 +432,47 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
                         }
                     }
                 }
-                if (valid) {
+                uint4 v[4];
+#pragma unroll
+                for (int x = 0; x < 4; ++x) {
+                    v[x].x = pack_bf16(__uint_as_float(orr[8 * x + 0]) * inv_l, __uint_as_float(orr[8 * x + 1]) * inv_l);
+                    v[x].y = pack_bf16(__uint_as_float(orr[8 * x + 2]) * inv_l, __uint_as_float(orr[8 * x + 3]) * inv_l);
+                    v[x].z = pack_bf16(__uint_as_float(orr[8 * x + 4]) * inv_l, __uint_as_float(orr[8 * x + 5]) * inv_l);
+                    v[x].w = pack_bf16(__uint_as_float(orr[8 * x + 6]) * inv_l, __uint_as_float(orr[8 * x + 7]) * inv_l);
+                }
+                if (a.o_tma) {
+                    // stage the row in SW128 layout over the drained K/V ring (every MMA has
+                    // completed once o_full fired); TMA bulk stores below
+                    uint8_t* panel = smem + SM::kv_off + t * kTileBytes + (cc >> 1) * kPanelBytes;
+#pragma unroll
+                    for (int x = 0; x < 4; ++x)
+                        *reinterpret_cast<uint4*>(panel + sw128_offset(row, (cc & 1) * 32 + 8 * x)) = v[x];
+                } else if (valid) {
                     uint4* dst = reinterpret_cast<uint4*>(orow + cc * 32);
 #pragma unroll
-                    for (int x = 0; x < 4; ++x) {
-                        uint4 v;
-                        v.x = pack_bf16(__uint_as_float(orr[8 * x + 0]) * inv_l, __uint_as_float(orr[8 * x + 1]) * inv_l);
-                        v.y = pack_bf16(__uint_as_float(orr[8 * x + 2]) * inv_l, __uint_as_float(orr[8 * x + 3]) * inv_l);
-                        v.z = pack_bf16(__uint_as_float(orr[8 * x + 4]) * inv_l, __uint_as_float(orr[8 * x + 5]) * inv_l);
-                        v.w = pack_bf16(__uint_as_float(orr[8 * x + 6]) * inv_l, __uint_as_float(orr[8 * x + 7]) * inv_l);
-                        dst[x] = v;
-                    }
+                    for (int x = 0; x < 4; ++x) dst[x] = v[x];
                 }
+            }
+        }
+        if (threadIdx.x == 128) TRACE(6);  // O read out of TMEM + staged
+        if (a.o_tma) {
+            // coalesced epilogue: one thread stores the staged (128 x 128) tiles; rows beyond
+            // q_len are clipped by the tensor maps (the scattered 16-B row stores of the
+            // previous epilogue took 3.3 us per CTA, profiles/r1_fa_variants.md)
+            fence_proxy_async_smem();
+            named_bar_sync(1, 128);
+            if (row == 0) {
+#pragma unroll
+                for (int t = 0; t < NO; ++t) {
+                    const uint8_t* tile = smem + SM::kv_off + t * kTileBytes;
+                    // out0 (aL): box (64, 1 frame, 128 rows) at (c, seg, row0);
+                    // out1 (y) : box (64, 128 rows, 1 frame) at (c, row0, seg)
+                    const int c1 = t == 0 ? seg : qtile * kTile, c2 = t == 0 ? qtile * kTile : seg;
+                    tma_store_5d(&a.tmO[t], tile, 0, c1, c2, 0, u);
+                    tma_store_5d(&a.tmO[t], tile + kPanelBytes, 64, c1, c2, 0, u);
+                }
+                tma_store_commit();
+                tma_store_wait_read();
             }
         }
         if (valid) {
@@ -441,6 +493,9 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc<512>(tmem);
+    }
+    if (threadIdx.x == 128) {
+        TRACE(7);  // epilogue done, CTA exiting
     }
 }
 
@@ -498,3 +553,10 @@ void tc_fa_launch(const TcFaArgs& a, int64_t U, cudaStream_t s) {
 }
 
 }  // namespace vmb
+
+#if VMB_TRACE
+extern "C" int vmb_debug_trace_read(unsigned long long* host, int ctas) {
+    const int n = ctas < 4096 ? ctas : 4096;
+    return cudaMemcpyFromSymbol(host, vmb::g_trace, sizeof(unsigned long long) * 8 * n) == cudaSuccess ? n : -1;
+}
+#endif

@@ -120,8 +120,8 @@ CUtensorMap make_tmap_bf16_5d(const void* base, const uint64_t dims[5], const ui
 
 int attn_impl(bool rstep) {
     // Kernel family per call site (A/B switches for measurements):
-    //   R half-steps (VMB_RSTEP): 2 = fa2 (default: 2 CTAs/SM, 64-key tiles) with fa_tc for
-    //     the last (y-fused) step, 1 = fa_tc for both, 4 = fa4 persistent for both
+    //   R half-steps (VMB_RSTEP): 2 = fa2 (default: 2 CTAs/SM, 64-key tiles) with the
+    //     persistent fa4 for the last (y-fused) step, 1 = fa_tc for both, 4 = fa4 for both
     //     (profiles/r1_fa_variants.md has the measurements behind the default)
     //   attention over all N keys: recompute / flash / dense (VMB_ATTN): 3 = fa3 (default),
     //     4 = fa4 persistent, 2 = fa2
@@ -448,9 +448,16 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
                 qv.base = ws.aR; qv.B = m * bq * d; qv.H = 0; qv.S = bq * d; qv.R = d; qv.Hn = 1;
             }
             if (last) {
-                // last R half-step with y = R V fused: O = P [K | V]
-                if (attn_impl(true) == 4) tc4_fa_launch(to_tc4(fa, qv), U, st);
-                else tc_fa_launch(fa, U, st);
+                // last R half-step with y = R V fused: O = P [K | V]; fa4 (persistent, epilogue
+                // warpgroup) unless VMB_RSTEP=1 forces the 1-CTA/SM fa_tc
+                if (attn_impl(true) != 1) {
+                    tc4_fa_launch(to_tc4(fa, qv), U, st);
+                } else {
+                    fa.o_tma = 1;
+                    fa.tmO[0] = internal_map(ws.aL, U, bq, m, d, true, 1, 128);  // aL (d, k, i, 1, U)
+                    fa.tmO[1] = internal_map(ws.y, U, m, bq, d, true, 128, 1);   // y  (d, i, k, 1, U)
+                    tc_fa_launch(fa, U, st);
+                }
             } else {
                 // R half-step without y: the 2-CTA/SM kernel (value operand = key tile)
                 Tc2Args f2{};
