@@ -179,8 +179,14 @@ struct Tc2Args {
     int32_t max_split;           // 1 disables split-KV
     int32_t nsplit;              // set by the launcher
     int64_t n_useg;              // set by the launcher
+    int32_t out_align32;         // set by the launcher: every output row 32-B aligned (256-bit stores)
 };
 int tc2_kv_tile(int nv);
+// 32-byte alignment of every bf16 output row of an attention launch (256-bit epilogue stores)
+inline bool rows_align32(const void* base, int64_t oB, int64_t oH, int64_t oS, int64_t oR) {
+    return reinterpret_cast<uintptr_t>(base) % 32 == 0 && oB % 16 == 0 && oH % 16 == 0 && oS % 16 == 0 &&
+           oR % 16 == 0;
+}
 int tc2_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg, int nv, int max_split);
 // Largest split count tc2_fa_launch may pick (sizes the partial buffers).
 constexpr int kTc2MaxSplit = 16;
@@ -223,6 +229,7 @@ struct Tc4Args {
     const void* q_rows;
     int64_t qrB, qrH, qrS, qrR;
     int32_t qrHn;
+    int32_t out_align32;         // every output row 32-byte aligned: 256-bit epilogue stores
 };
 int tc4_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg, int max_split);
 void tc4_fa_launch(Tc4Args a, int64_t U, cudaStream_t s);

@@ -383,11 +383,20 @@ __global__ void __launch_bounds__(kThreads, 2) fa2_kernel(const __grid_constant_
                 VMB_TMEM_LD32(tO + cc * 32 + lane_base, orr);
                 tmem_ld_wait();
                 if (valid) {
-                    float4* dst = reinterpret_cast<float4*>(prow + cc * 32);
+                    // fp32 partial rows (512 B, 32-B aligned workspace): 256-bit stores
 #pragma unroll
-                    for (int x = 0; x < 8; ++x)
-                        dst[x] = make_float4(__uint_as_float(orr[4 * x + 0]) * inv_l, __uint_as_float(orr[4 * x + 1]) * inv_l,
-                                             __uint_as_float(orr[4 * x + 2]) * inv_l, __uint_as_float(orr[4 * x + 3]) * inv_l);
+                    for (int x = 0; x < 4; ++x) {
+                        uint4 lo, hi;
+                        lo.x = __float_as_uint(__uint_as_float(orr[8 * x + 0]) * inv_l);
+                        lo.y = __float_as_uint(__uint_as_float(orr[8 * x + 1]) * inv_l);
+                        lo.z = __float_as_uint(__uint_as_float(orr[8 * x + 2]) * inv_l);
+                        lo.w = __float_as_uint(__uint_as_float(orr[8 * x + 3]) * inv_l);
+                        hi.x = __float_as_uint(__uint_as_float(orr[8 * x + 4]) * inv_l);
+                        hi.y = __float_as_uint(__uint_as_float(orr[8 * x + 5]) * inv_l);
+                        hi.z = __float_as_uint(__uint_as_float(orr[8 * x + 6]) * inv_l);
+                        hi.w = __float_as_uint(__uint_as_float(orr[8 * x + 7]) * inv_l);
+                        st_global_256(prow + cc * 32 + 8 * x, lo, hi);
+                    }
                 }
             }
             if (valid) a.part_lse[((int64_t)useg * a.nsplit + split) * a.q_len + grow] = kLn2 * lse2;
@@ -414,15 +423,21 @@ __global__ void __launch_bounds__(kThreads, 2) fa2_kernel(const __grid_constant_
                     }
                 }
                 if (valid) {
-                    uint4* dst = reinterpret_cast<uint4*>(orow + cc * 32);
+                    uint4 v[4];
 #pragma unroll
                     for (int x = 0; x < 4; ++x) {
-                        uint4 v;
-                        v.x = pack_bf16(__uint_as_float(orr[8 * x + 0]) * inv_l, __uint_as_float(orr[8 * x + 1]) * inv_l);
-                        v.y = pack_bf16(__uint_as_float(orr[8 * x + 2]) * inv_l, __uint_as_float(orr[8 * x + 3]) * inv_l);
-                        v.z = pack_bf16(__uint_as_float(orr[8 * x + 4]) * inv_l, __uint_as_float(orr[8 * x + 5]) * inv_l);
-                        v.w = pack_bf16(__uint_as_float(orr[8 * x + 6]) * inv_l, __uint_as_float(orr[8 * x + 7]) * inv_l);
-                        dst[x] = v;
+                        v[x].x = pack_bf16(__uint_as_float(orr[8 * x + 0]) * inv_l, __uint_as_float(orr[8 * x + 1]) * inv_l);
+                        v[x].y = pack_bf16(__uint_as_float(orr[8 * x + 2]) * inv_l, __uint_as_float(orr[8 * x + 3]) * inv_l);
+                        v[x].z = pack_bf16(__uint_as_float(orr[8 * x + 4]) * inv_l, __uint_as_float(orr[8 * x + 5]) * inv_l);
+                        v[x].w = pack_bf16(__uint_as_float(orr[8 * x + 6]) * inv_l, __uint_as_float(orr[8 * x + 7]) * inv_l);
+                    }
+                    if (a.out_align32) {  // 256-bit stores: one full sector per instruction
+                        st_global_256(orow + cc * 32, v[0], v[1]);
+                        st_global_256(orow + cc * 32 + 16, v[2], v[3]);
+                    } else {
+                        uint4* dst = reinterpret_cast<uint4*>(orow + cc * 32);
+#pragma unroll
+                        for (int x = 0; x < 4; ++x) dst[x] = v[x];
                     }
                 }
             }
@@ -518,6 +533,7 @@ void tc2_fa_launch(Tc2Args a, int64_t U, cudaStream_t s) {
     p.total_tiles = total_tiles;
     a.nsplit = nsplit;
     a.n_useg = n_useg;
+    a.out_align32 = rows_align32(a.out, a.oB, a.oH, a.oS, a.oR) ? 1 : 0;
     p.a = a;
     if (nsplit == 1) p.a.part_o = nullptr;
     if (a.nv == 1) launch<1>(p, n_useg, nsplit, s);

@@ -539,15 +539,21 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                             }
                         }
                         if (valid) {
-                            uint4* dst = reinterpret_cast<uint4*>(orow + cc * 32);
+                            uint4 v[4];
 #pragma unroll
                             for (int x = 0; x < 4; ++x) {
-                                uint4 v;
-                                v.x = pack_bf16(__uint_as_float(orr[8 * x + 0]) * inv_l, __uint_as_float(orr[8 * x + 1]) * inv_l);
-                                v.y = pack_bf16(__uint_as_float(orr[8 * x + 2]) * inv_l, __uint_as_float(orr[8 * x + 3]) * inv_l);
-                                v.z = pack_bf16(__uint_as_float(orr[8 * x + 4]) * inv_l, __uint_as_float(orr[8 * x + 5]) * inv_l);
-                                v.w = pack_bf16(__uint_as_float(orr[8 * x + 6]) * inv_l, __uint_as_float(orr[8 * x + 7]) * inv_l);
-                                dst[x] = v;
+                                v[x].x = pack_bf16(__uint_as_float(orr[8 * x + 0]) * inv_l, __uint_as_float(orr[8 * x + 1]) * inv_l);
+                                v[x].y = pack_bf16(__uint_as_float(orr[8 * x + 2]) * inv_l, __uint_as_float(orr[8 * x + 3]) * inv_l);
+                                v[x].z = pack_bf16(__uint_as_float(orr[8 * x + 4]) * inv_l, __uint_as_float(orr[8 * x + 5]) * inv_l);
+                                v[x].w = pack_bf16(__uint_as_float(orr[8 * x + 6]) * inv_l, __uint_as_float(orr[8 * x + 7]) * inv_l);
+                            }
+                            if (a.out_align32) {
+                                st_global_256(orow + cc * 32, v[0], v[1]);
+                                st_global_256(orow + cc * 32 + 16, v[2], v[3]);
+                            } else {
+                                uint4* dst = reinterpret_cast<uint4*>(orow + cc * 32);
+#pragma unroll
+                                for (int x = 0; x < 4; ++x) dst[x] = v[x];
                             }
                         }
                     }
@@ -610,6 +616,16 @@ void tc4_fa_launch(Tc4Args a, int64_t U, cudaStream_t s) {
     p.nsplit = (a.part_o && a.nv == 1 && !a.v_is_k) ? tc4_plan_splits(a.q_len, a.kv_len, n_useg, a.max_split) : 1;
     p.n_kv_tiles = (p.total_tiles + p.nsplit - 1) / p.nsplit;
     p.n_items = (int64_t)p.q_tiles * p.nsplit * n_useg;
+    {
+        // 256-bit stores need every output row 32-byte aligned
+        bool al = true;
+        for (int t = 0; t < a.nv && t < 2; ++t) {
+            void* base = t == 0 ? a.out0 : a.out1;
+            al = al && (reinterpret_cast<uintptr_t>(base) % 32 == 0) && a.oB[t] % 16 == 0 && a.oH[t] % 16 == 0 &&
+                 a.oS[t] % 16 == 0 && a.oR[t] % 16 == 0;
+        }
+        a.out_align32 = al ? 1 : 0;
+    }
     VMB_REQUIRE_DIM(p.n_items < ((int64_t)1 << 31), "too many work items for one launch");
     a.nsplit = p.nsplit;
     if (p.nsplit == 1) a.part_o = nullptr;

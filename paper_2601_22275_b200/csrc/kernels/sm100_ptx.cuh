@@ -296,6 +296,15 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// 256-bit global store (sm_100 STG.256): one 32-byte sector per thread instead of two
+// half-sector 16-byte stores -- halves the L1/L2 transactions of row-per-thread epilogues.
+// `p` must be 32-byte aligned.
+__device__ __forceinline__ void st_global_256(void* p, const uint4& a, const uint4& b) {
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(a.x), "r"(a.y),
+                 "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+                 : "memory");
+}
+
 // Byte offset of element (row, col) inside a [rows x 64] bf16 SW128 panel
 // (16-byte chunk index XOR row%8), matching TMA SWIZZLE_128B / UMMA SWIZZLE_128B.
 __device__ __forceinline__ uint32_t sw128_offset(uint32_t row, uint32_t col) {
