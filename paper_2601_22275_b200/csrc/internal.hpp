@@ -197,6 +197,10 @@ void tc2_combine_launch(const Tc2Args& a, cudaStream_t s);
 // (K/V maps with box rows 128).  Same argument block as fa2.
 int tc3_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg, int max_split);
 void tc3_fa_launch(Tc2Args a, int64_t U, cudaStream_t s);
+// fa5_tc.cu: persistent fa3 (two query tiles per item, ping-pong softmax warpgroups, one CTA
+// per SM over a flattened item stream); same argument block and 128-key K/V boxes.
+int tc5_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg, int max_split);
+void tc5_fa_launch(Tc2Args a, int64_t U, cudaStream_t s);
 // fa4_tc.cu: persistent (one CTA per SM) flash attention over a flattened stream of
 // (query tile, segment, kv-split) items; 128-key tiles (K/V maps with box rows 128).
 //   nv = 1, v_is_k = 1: R half-step (out0 = aL, cl_out)

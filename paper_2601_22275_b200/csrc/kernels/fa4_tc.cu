@@ -158,8 +158,12 @@ __device__ __forceinline__ void trace4(int n, int ev) {
     }
 }
 #define TRACE4(n, ev) trace4(n, ev)
+__device__ long long g_trace4t[16][2][12][6];
+#define TRACE4T(n, j, ev) do { if (threadIdx.x == 128 && blockIdx.x < 16 && (n) >= 1 && (n) <= 2 && (j) < 12) \
+    g_trace4t[blockIdx.x][(n) - 1][(j)][(ev)] = clock64(); } while (0)
 #else
 #define TRACE4(n, ev) do { } while (0)
+#define TRACE4T(n, j, ev) do { } while (0)
 #endif
 
 template <int NB, int NO>
@@ -358,13 +362,16 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
             if (threadIdx.x == 128) TRACE4(n, 0);
             for (int j = 0; j < w.n_kv; ++j, ++g) {
                 const uint32_t tS = tS0 + (uint32_t)(g & 1) * 128 + lane_base;
+                TRACE4T(n, j, 0);
                 mbar_wait_sleep(&s_full[g & 1], (g >> 1) & 1);
+                TRACE4T(n, j, 1);
                 if (threadIdx.x == 128 && j == 0) TRACE4(n, 1);
                 tc_fence_after();
                 uint32_t sr[64];
                 VMB_TMEM_LD32(tS + 64 * h + 0, (sr + 0));
                 VMB_TMEM_LD32(tS + 64 * h + 32, (sr + 32));
                 tmem_ld_wait();
+                TRACE4T(n, j, 2);
                 float* s = reinterpret_cast<float*>(sr);
                 if (j == w.n_kv - 1 && last_valid < 64) {
                     asm volatile("");  // keep this a real (rarely taken) branch, not 64 selects
@@ -386,6 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                 __nv_bfloat16* slot = xch + (g & 1) * 256;
                 slot[h * 128 + row] = __float2bfloat16_ru(fmaxf(fmaxf(a0, a1), fmaxf(a2, a3)));
                 named_bar_sync(1, 256);
+                TRACE4T(n, j, 3);
                 const float m_cand = fmaxf(__bfloat162float(slot[row]), __bfloat162float(slot[128 + row])) * scale2;
                 bool rescale = false;
                 float alpha = 1.f;
@@ -438,9 +446,11 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                         VMB_TMEM_ST32(ta, orr);
                     }
                 }
+                TRACE4T(n, j, 4);
                 tmem_st_wait();
                 tc_fence_before();
                 mbar_arrive(&p_full[g & 1]);
+                TRACE4T(n, j, 5);
             }
             if (threadIdx.x == 128) TRACE4(n, 2);
             // hand the item's row statistics to the epilogue warpgroup and move on
@@ -652,6 +662,9 @@ void tc4_fa_launch(Tc4Args a, int64_t U, cudaStream_t s) {
 }  // namespace vmb
 
 #if VMB_TRACE
+extern "C" int vmb_debug_trace4t_read(long long* host) {
+    return cudaMemcpyFromSymbol(host, vmb::g_trace4t, sizeof(long long) * 16 * 2 * 12 * 6) == cudaSuccess ? 0 : -1;
+}
 extern "C" int vmb_debug_trace4_read(unsigned long long* host) {
     return cudaMemcpyFromSymbol(host, vmb::g_trace4, sizeof(unsigned long long) * 64 * 16 * 8) == cudaSuccess ? 0 : -1;
 }

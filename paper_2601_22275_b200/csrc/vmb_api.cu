@@ -121,19 +121,20 @@ CUtensorMap make_tmap_bf16_5d(const void* base, const uint64_t dims[5], const ui
 int attn_impl(bool rstep) {
     // Kernel family per call site (A/B switches for measurements):
     //   R half-steps (VMB_RSTEP): 2 = fa2 (default: 2 CTAs/SM, 64-key tiles) with the
-    //     persistent fa4 for the last (y-fused) step, 1 = fa_tc for both, 4 = fa4 for both
+    //     persistent fa4 for the last (y-fused) step, 1 = fa_tc for both, 4 = fa4 for both,
+    //     5 = persistent 2-Q-tile fa5 (+ fa4 for the last step)
     //     (profiles/r1_fa_variants.md has the measurements behind the default)
     //   attention over all N keys: recompute / flash / dense (VMB_ATTN): 3 = fa3 (default),
-    //     4 = fa4 persistent, 2 = fa2
+    //     4 = fa4 persistent, 5 = fa5 persistent 2-Q-tile, 2 = fa2
     static const int r = [] {
         const char* e = getenv("VMB_RSTEP");
         const int v = e ? atoi(e) : 2;
-        return (v == 1 || v == 4) ? v : 2;
+        return (v == 1 || v == 4 || v == 5) ? v : 2;
     }();
     static const int at = [] {
         const char* e = getenv("VMB_ATTN");
         const int v = e ? atoi(e) : 3;
-        return (v == 2 || v == 4) ? v : 3;
+        return (v == 2 || v == 4 || v == 5) ? v : 3;
     }();
     return rstep ? r : at;
 }
@@ -148,6 +149,7 @@ int attn_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg) {
     switch (attn_impl(false)) {
         case 2: return tc2_plan_splits(q_len, kv_len, n_useg, 2, kTc2MaxSplit);
         case 4: return tc4_plan_splits(q_len, kv_len, n_useg, kTc2MaxSplit);
+        case 5: return tc5_plan_splits(q_len, kv_len, n_useg, kTc2MaxSplit);
         default: return tc3_plan_splits(q_len, kv_len, n_useg, kTc2MaxSplit);
     }
 }
@@ -195,6 +197,7 @@ void attn_launch(const Tc2Args& a, int64_t U, cudaStream_t s, bool rstep, const 
     switch (attn_impl(rstep)) {
         case 2: tc2_fa_launch(a, U, s); break;
         case 4: tc4_fa_launch(to_tc4(a, qv), U, s); break;
+        case 5: tc5_fa_launch(a, U, s); break;
         case 1:  // original 1-CTA/SM kernel (R half-step only)
         default:
             if (rstep && attn_impl(true) == 1) {

@@ -34,3 +34,14 @@ per_item = np.diff(t[:, 1:15, 0], axis=1)
 print(f"  item period (start to next start): {per_item.mean():.2f} us")
 wait_s0 = t[:, 1:15, 1] - t[:, 1:15, 0]
 print(f"  wait for S0 at item start: {wait_s0.mean():.2f} us")
+
+# fine-grained softmax tile phases (clock64 cycles), warp 4 lane 0, items 1-2, tiles 0-11
+tb = (C.c_longlong * (16 * 2 * 12 * 6))()
+vm.lib.vmb_debug_trace4t_read.argtypes = [C.c_void_p]
+vm.lib.vmb_debug_trace4t_read(C.addressof(tb))
+tt = np.frombuffer(tb, dtype=np.int64).reshape(16, 2, 12, 6).astype(np.float64)
+ph = ["wait S", "TMEM ld", "max+xchg", "exp/P st", "st wait+arrive"]
+d = np.diff(tt, axis=3)[:, :, 1:11]  # tiles 1..10
+print("softmax tile phases (cycles, mean over CTAs/items/tiles):", {ph[i]: round(float(d[..., i].mean())) for i in range(5)})
+per = np.diff(tt[:, :, :, 0], axis=2)[:, :, 1:10]
+print("softmax tile period (cycles):", round(float(per.mean())))
