@@ -259,6 +259,8 @@ struct TcLstepArgs {
     float out_scale;    // multiplies the epilogue (ITER: aR scale)
 };
 void tc_lstep_launch(const TcLstepArgs& a, int64_t U, cudaStream_t s);
+// lstep_p.cu: persistent, pipelined variant (producer warp + TMA ring, two consumer warpgroups)
+void tc_lstep_p_launch(const TcLstepArgs& a, int64_t U, cudaStream_t s);
 
 // seq_gather.cu: sequence-sharded K/V layout
 constexpr int kMaxSeqRanks = 64;

@@ -502,7 +502,14 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
             ls.final_mode = last;
             ls.cR = ws.cR;
             ls.out_scale = last ? 1.f : qscale;
-            tc_lstep_launch(ls, U, st);
+            // one position per CTA (4 CTAs/SM) unless VMB_LSTEP=2 selects the persistent pipelined
+            // kernel (measured slower: 1.10 vs 0.85 ms at C4, profiles/r1_fa_variants.md)
+            static const bool lstep_pipelined = [] {
+                const char* e = getenv("VMB_LSTEP");
+                return e && e[0] == '2';
+            }();
+            if (lstep_pipelined) tc_lstep_p_launch(ls, U, st);
+            else tc_lstep_launch(ls, U, st);
         }
         if (recompute) {
             // first-frame recompute: Q[0:hw) against all N keys, split over the keys
