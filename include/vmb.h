@@ -152,6 +152,12 @@ vmb_status vmb_flash_entropy_fwd(int64_t units, int64_t nq, int64_t nk, int64_t 
 vmb_status vmb_dense_fwd(int64_t units, int64_t n, int64_t d, vmb_dtype dtype, const void* q,
                          const void* k, const void* v, void* o, void* stream);
 
+/* ---- caller-side harness (host only) ----
+ * The reference bench's workload generator (bench_main.cpp:78-90): count values from
+ * std::mt19937_64(seed) through normal_distribution<double>(0,1) (dist 0) or
+ * uniform_real_distribution<double>(-1,1) (dist 1), cast to float (host buffer). */
+vmb_status vmb_workload_fill(uint64_t seed, int64_t count, int32_t dist, float* out);
+
 /* ---- diagnostics ---- */
 /* Number of kernels the library launched since load (all entry points). */
 uint64_t vmb_kernel_launch_count(void);

@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <random>
 #include <vector>
 
 #include "internal.hpp"
@@ -1049,6 +1050,25 @@ int32_t vmb_profile_read(double* ms, uint64_t* counts, int32_t reset) {
         }
     }
     return kKNum;
+}
+
+// Caller-side harness: the reference bench's workload generator (bench_main.cpp:78-90,
+// 169-173): std::mt19937_64(seed) with normal_distribution<double>(0, 1) (dist 0) or
+// uniform_real_distribution<double>(-1, 1) (dist 1), cast to float.  Host code; the same
+// libstdc++ distributions, so inputs are bit-identical to the reference harness.
+vmb_status vmb_workload_fill(uint64_t seed, int64_t count, int32_t dist, float* out) {
+    return guarded([&] {
+        VMB_REQUIRE_DIM(count >= 0 && (count == 0 || out), "workload buffer");
+        VMB_REQUIRE_DIM(dist == 0 || dist == 1, "dist must be 0 (normal) or 1 (uniform)");
+        std::mt19937_64 rng(seed);
+        if (dist == 1) {
+            std::uniform_real_distribution<double> ud(-1.0, 1.0);
+            for (int64_t i = 0; i < count; ++i) out[i] = static_cast<float>(ud(rng));
+        } else {
+            std::normal_distribution<double> nd(0.0, 1.0);
+            for (int64_t i = 0; i < count; ++i) out[i] = static_cast<float>(nd(rng));
+        }
+    });
 }
 
 vmb_status vmb_selftest_umma(int32_t mode, const void* A, const void* B, float* C, void* stream) {
