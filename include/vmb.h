@@ -148,6 +148,16 @@ vmb_status vmb_flash_entropy_fwd(int64_t units, int64_t nq, int64_t nk, int64_t 
                                  vmb_dtype dtype, const void* q, const void* k, const void* v,
                                  float q_scale, void* o, float* lse, float* ent, void* stream);
 
+/* ---- its backward (flash_entropy.hpp:146-221; the paper's fine-tuning path, Alg. 2) ----
+ * q (pre-scaled), k, v, o, dout (units, n, d) dtype; lse / ent / dent (units, nq) f32 from the
+ * matching forward (ent, dent may be NULL unless entropy_grad).  dq (units, nq, d), dk / dv
+ * (units, nk, d) in dtype are overwritten.  entropy_grad adds -dH P (S - lse + H) to dS. */
+vmb_status vmb_flash_entropy_bwd(int64_t units, int64_t nq, int64_t nk, int64_t d, vmb_dtype dtype,
+                                 const void* q, const void* k, const void* v, const void* o,
+                                 const void* dout, const float* lse, const float* ent,
+                                 const float* dent, int32_t entropy_grad, void* dq, void* dk,
+                                 void* dv, void* stream);
+
 /* ---- dense attention baseline (oracle.hpp:36-72 semantics, scale 1/sqrt(d)) ---- */
 vmb_status vmb_dense_fwd(int64_t units, int64_t n, int64_t d, vmb_dtype dtype, const void* q,
                          const void* k, const void* v, void* o, void* stream);

@@ -144,6 +144,22 @@ class Oracle:
         self._check(st, "flash_entropy_fwd")
         return out, lse, ent
 
+    def flash_entropy_bwd(self, q, k, v, o, dout, lse, ent=None, dent=None, entropy_grad=False, br=64, bc=64):
+        """flash_entropy.hpp:146-221 -> (dq, dk, dv)."""
+        dt = q.dtype
+        nq, d = q.shape
+        nk = k.shape[0]
+        dq = np.zeros((nq, d), dt)
+        dk = np.zeros((nk, d), dt)
+        dv = np.zeros((nk, d), dt)
+        f = self._fn("flash_entropy_bwd_" + self._sfx(dt))
+        f.argtypes = [_P] * 8 + [_I64, _I64, _I64, _INT, _I64, _I64, _P, _P, _P]
+        c = lambda a: None if a is None else np.ascontiguousarray(a, dtype=dt)  # noqa: E731
+        ins = [c(q), c(k), c(v), c(o), c(dout), c(lse), c(ent), c(dent)]
+        st = f(*[_ptr(a) for a in ins], nq, nk, d, int(entropy_grad), br, bc, _ptr(dq), _ptr(dk), _ptr(dv))
+        self._check(st, "flash_entropy_bwd")
+        return dq, dk, dv
+
     def vmonarch_attention(self, q, k, v, grid, iters=2, clamp_min=0.1, clamp_enabled=True,
                            recompute=True, override=(0, 0), threads=1, tiles=(64, 64)):
         """q,k,v: (units, N, d).  grid = (T, h, w).  Returns (units, N, d)."""

@@ -134,6 +134,25 @@ int flash(const T* q, const T* k, const T* v, int64_t nq, int64_t nk, int64_t d,
     });
 }
 
+template <class T>
+int flash_bwd(const T* q, const T* k, const T* v, const T* o, const T* dout, const T* lse, const T* ent,
+              const T* dent, int64_t nq, int64_t nk, int64_t d, int eg, int64_t br, int64_t bc, T* dq, T* dk,
+              T* dv) {
+    return guarded([&] {
+        TileConfig tc;
+        tc.b_r = br;
+        tc.b_c = bc;
+        std::vector<T> l(lse, lse + nq), e, de;
+        if (ent) e.assign(ent, ent + nq);
+        if (dent) de.assign(dent, dent + nq);
+        auto r = flash_entropy_bwd(mat_from(q, nq, d), mat_from(k, nk, d), mat_from(v, nk, d), mat_from(o, nq, d),
+                                   mat_from(dout, nq, d), l, e, de, eg != 0, tc);
+        copy_out(r.dq.data, dq);
+        copy_out(r.dk.data, dk);
+        copy_out(r.dv.data, dv);
+    });
+}
+
 // video.hpp:84-150 over `units` independent (N, d) matrices laid out back to back.
 template <class T>
 int vmonarch_multi(int64_t units, const T* q, const T* k, const T* v, int64_t t_frames,
@@ -218,6 +237,12 @@ int vmr_flops_estimate(int64_t t_frames, int64_t h, int64_t w, int64_t om, int64
     int vmr_flash_entropy_fwd_##S(const T* q, const T* k, const T* v, int64_t nq, int64_t nk,  \
                                   int64_t d, int64_t br, int64_t bc, T* out, T* lse, T* ent) { \
         return flash<T>(q, k, v, nq, nk, d, br, bc, out, lse, ent);                             \
+    }                                                                                           \
+    int vmr_flash_entropy_bwd_##S(const T* q, const T* k, const T* v, const T* o, const T* dout, \
+                                  const T* lse, const T* ent, const T* dent, int64_t nq,       \
+                                  int64_t nk, int64_t d, int eg, int64_t br, int64_t bc, T* dq, \
+                                  T* dk, T* dv) {                                               \
+        return flash_bwd<T>(q, k, v, o, dout, lse, ent, dent, nq, nk, d, eg, br, bc, dq, dk, dv); \
     }                                                                                           \
     int vmr_vmonarch_attention_##S(int64_t units, const T* q, const T* k, const T* v,          \
                                    int64_t tf, int64_t h, int64_t w, int64_t d, int64_t iters, \

@@ -68,6 +68,11 @@ int vmo_flops_estimate(int64_t t_frames, int64_t h, int64_t w, int64_t om, int64
     int vmo_flash_entropy_fwd_##S(const T* q, const T* k, const T* v, int64_t nq,           \
                                   int64_t nk, int64_t d, int64_t br, int64_t bc, T* out,    \
                                   T* lse, T* ent);                                          \
+    /* flash_entropy.hpp:146-221 tiled backward (entropy_grad adds -dH P (S - lse + H)). */  \
+    int vmo_flash_entropy_bwd_##S(const T* q, const T* k, const T* v, const T* o,           \
+                                  const T* dout, const T* lse, const T* ent, const T* dent, \
+                                  int64_t nq, int64_t nk, int64_t d, int entropy_grad,      \
+                                  int64_t br, int64_t bc, T* dq, T* dk, T* dv);             \
     /* video.hpp:84-150 for ONE batch*head unit (units are independent, video.hpp:115).     \
      * override (om, ob) = (0,0) for the default factorization. */                          \
     int vmo_vmonarch_unit_##S(const T* q, const T* k, const T* v, int64_t t_frames,         \

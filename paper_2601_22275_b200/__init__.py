@@ -31,6 +31,7 @@ __all__ = [
     "vmonarch_attention", "r_update", "l_update", "flash_entropy_fwd", "dense_forward",
     "factorize", "flops_estimate", "make_perm", "preset_grid", "export_factors", "lib",
     "kernel_launch_count", "LIB_PATH", "vmonarch_attention_slab", "seq_assemble", "vmonarch_attention_host",
+    "flash_entropy_bwd",
 ]
 
 LIB_PATH = os.environ.get("VMB_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libvmb.so")
@@ -100,6 +101,7 @@ _vmb_export = _sig("vmb_export_factors", [C.POINTER(_Grid), C.POINTER(_Cfg), C.c
 _vmb_rstep = _sig("vmb_rstep", [_I64, _I64, _I64, _I64, C.c_int, _P, _P, _P, _D, _I32, _P, _P, _P, _P])
 _vmb_lstep = _sig("vmb_lstep", [_I64, _I64, _I64, _I64, C.c_int, _P, _P, _P, _P, _P, _P, _P])
 _vmb_flash = _sig("vmb_flash_entropy_fwd", [_I64, _I64, _I64, _I64, C.c_int, _P, _P, _P, _F, _P, _P, _P, _P])
+_vmb_flash_bwd = _sig("vmb_flash_entropy_bwd", [_I64, _I64, _I64, _I64, C.c_int] + [_P] * 8 + [_I32, _P, _P, _P, _P])
 _vmb_dense = _sig("vmb_dense_fwd", [_I64, _I64, _I64, C.c_int, _P, _P, _P, _P, _P])
 _vmb_launches = _sig("vmb_kernel_launch_count", [], C.c_uint64)
 _vmb_ws_size_seq = _sig("vmb_workspace_size_seq", [C.POINTER(_Grid), C.POINTER(_Cfg), C.c_int, _I64], C.c_size_t)
@@ -509,6 +511,42 @@ def flash_entropy_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, q_scale
     if squeeze:
         return o[0], lse[0], (ent[0] if ent is not None else None)
     return o, lse, ent
+
+
+def flash_entropy_bwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor, dout: torch.Tensor,
+                      lse: torch.Tensor, entropy: Optional[torch.Tensor] = None,
+                      dentropy: Optional[torch.Tensor] = None, entropy_grad: bool = False):
+    """flash_entropy.hpp:146-221 (Alg. 2): (dq, dk, dv) for (units, n, d) or (n, d) inputs.
+    q must be the pre-scaled query of the matching flash_entropy_fwd; lse / entropy come from
+    that forward; entropy_grad adds the -dH P (S - lse + H) correction to dS."""
+    _require_cuda(q, k, v, o, dout, lse, entropy, dentropy)
+    squeeze = q.dim() == 2
+    if squeeze:
+        q, k, v, o, dout = q[None], k[None], v[None], o[None], dout[None]
+        lse = lse[None]
+        entropy = entropy[None] if entropy is not None else None
+        dentropy = dentropy[None] if dentropy is not None else None
+    U, nq, d = q.shape
+    nk = k.shape[1]
+    if k.shape[2] != d or v.shape[2] != d or o.shape[2] != d or dout.shape[2] != d:
+        raise DimensionError("dimension error: all operands must share head dim")
+    if v.shape[1] != nk:
+        raise DimensionError("dimension error: K and V must share row count")
+    if o.shape[1] != nq or dout.shape[1] != nq:
+        raise DimensionError("dimension error: O and dO must have N_q rows")
+    if lse.shape[-1] != nq or (entropy is not None and entropy.shape[-1] != nq) or \
+            (dentropy is not None and dentropy.shape[-1] != nq):
+        raise DimensionError("dimension error: lse / entropy / dH length must equal N_q")
+    dt = _dtype_code(q)
+    q, k, v, o, dout = (x.contiguous().to(q.dtype) for x in (q, k, v, o, dout))
+    f32 = lambda x: None if x is None else x.contiguous().float()  # noqa: E731
+    lse, entropy, dentropy = f32(lse), f32(entropy), f32(dentropy)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    _check(_vmb_flash_bwd(U, nq, nk, d, dt, _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(dout), _ptr(lse), _ptr(entropy),
+                          _ptr(dentropy), int(entropy_grad), _ptr(dq), _ptr(dk), _ptr(dv), _stream()))
+    if squeeze:
+        return dq[0], dk[0], dv[0]
+    return dq, dk, dv
 
 
 def dense_forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor) -> torch.Tensor:

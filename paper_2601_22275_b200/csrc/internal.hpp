@@ -262,6 +262,12 @@ void tc_lstep_launch(const TcLstepArgs& a, int64_t U, cudaStream_t s);
 // lstep_p.cu: persistent, pipelined variant (producer warp + TMA ring, two consumer warpgroups)
 void tc_lstep_p_launch(const TcLstepArgs& a, int64_t U, cudaStream_t s);
 
+// flash_bwd.cu: backward of the online-entropy attention (flash_entropy.hpp:146-221)
+void flash_bwd_launch(int64_t U, int64_t nq, int64_t nk, int64_t d, bool bf16, const void* q, const void* k,
+                      const void* v, const void* o, const void* dout, const float* lse, const float* ent,
+                      const float* dent, int entropy_grad, float* dvec, void* dq, void* dk, void* dv,
+                      cudaStream_t s);
+
 // seq_gather.cu: sequence-sharded K/V layout
 constexpr int kMaxSeqRanks = 64;
 void seq_assemble(const void* gathered, void* full, int64_t units, int64_t T, int64_t hw, int64_t slab_max,

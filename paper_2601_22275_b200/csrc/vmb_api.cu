@@ -1014,6 +1014,26 @@ vmb_status vmb_flash_entropy_fwd(int64_t units, int64_t nq, int64_t nk, int64_t 
     });
 }
 
+vmb_status vmb_flash_entropy_bwd(int64_t units, int64_t nq, int64_t nk, int64_t d, vmb_dtype dtype, const void* q,
+                                 const void* k, const void* v, const void* o, const void* dout, const float* lse,
+                                 const float* ent, const float* dent, int32_t entropy_grad, void* dq, void* dk,
+                                 void* dv, void* stream) {
+    return guarded([&] {
+        VMB_REQUIRE_DIM(units >= 0 && nq >= 0 && d >= 1, "bad attention shape");
+        VMB_REQUIRE_DIM(dtype == VMB_F32 || dtype == VMB_BF16, "unsupported dtype");
+        VMB_REQUIRE_DIM(!entropy_grad || (ent && dent), "entropy_grad requires entropy and dH inputs");
+        VMB_REQUIRE_DOMAIN(nk >= 1, "attention over empty keys");
+        VMB_REQUIRE_DIM(units * nq == 0 || (q && o && dout && lse && dq), "null tensor pointer");
+        VMB_REQUIRE_DIM(k && v && dk && dv, "null tensor pointer");
+        cudaStream_t st = as_stream(stream);
+        float* dvec = nullptr;
+        if (units * nq > 0) VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dvec), sizeof(float) * units * nq, st));
+        flash_bwd_launch(units, nq, nk, d, dtype == VMB_BF16, q, k, v, o, dout, lse, ent, dent, entropy_grad, dvec, dq,
+                         dk, dv, st);
+        if (dvec) VMB_CHECK_CUDA(cudaFreeAsync(dvec, st));
+    });
+}
+
 vmb_status vmb_dense_fwd(int64_t units, int64_t n, int64_t d, vmb_dtype dtype, const void* q, const void* k,
                          const void* v, void* o, void* stream) {
     return vmb_flash_entropy_fwd(units, n, n, d, dtype, q, k, v, (float)(1.0 / std::sqrt((double)d)), o, nullptr,

@@ -122,3 +122,19 @@ def test_bf16_round_matches_torch():
     import torch
     x = randn((1000,), 5, sigma=3.0, dtype=np.float32)
     assert np.array_equal(bf16_round(x), torch.from_numpy(x).bfloat16().float().numpy())
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("eg", [False, True])
+def test_port_flash_bwd_equals_reference(orc, ref, dtype, eg):
+    """flash_entropy.hpp:146-221: the C restatement of the backward is bit-exact."""
+    q = randn((24, 6), 1, dtype=dtype)
+    k = randn((30, 6), 2, dtype=dtype)
+    v = randn((30, 6), 3, dtype=dtype)
+    g = randn((24, 6), 4, dtype=dtype)
+    dh = randn((24,), 5, dtype=dtype)
+    o, lse, ent = ref.flash_entropy_fwd(q, k, v, br=8, bc=8)
+    a = orc.flash_entropy_bwd(q, k, v, o, g, lse, ent, dh, eg, br=8, bc=8)
+    b = ref.flash_entropy_bwd(q, k, v, o, g, lse, ent, dh, eg, br=8, bc=8)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
