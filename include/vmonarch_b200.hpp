@@ -1,7 +1,12 @@
 // vmonarch_b200.hpp — C++ drop-in façade over the libvmb C ABI (include/vmb.h).
 //
 // Same call shape, argument meaning and exception types as the reference operator
-// (/root/reference/proj/include/vmonarch/video.hpp:84-150, check.hpp:10-20):
+// (/root/reference/proj/include/vmonarch/video.hpp:84-150, check.hpp:10-20) and its
+// companions monarch_attention (monarch.hpp:155-193), flash_entropy_fwd / _bwd
+// (flash_entropy.hpp:85-221), dense_forward (oracle.hpp:36-72), factorize / flops_estimate
+// (video.cpp:13-59); where the reference returns its own aggregate (MonarchResult,
+// FlashFwdResult, FlashBwdResult, CostReport) the caller names that type as the first
+// template argument, e.g. vmonarch_b200::flash_entropy_fwd<vmonarch::FlashFwdResult<float>>(...):
 //
 //   // reference                                   // here (B200)
 //   vmonarch::vmonarch_attention<float>(            vmonarch_b200::vmonarch_attention(
@@ -25,7 +30,9 @@
 
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
+#include <utility>
 #include <cstring>
 #include <span>
 #include <stdexcept>
@@ -68,6 +75,10 @@ public:
     }
     DeviceBuffer(const DeviceBuffer&) = delete;
     DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+    DeviceBuffer(DeviceBuffer&& o) noexcept : ptr_(o.ptr_), bytes_(o.bytes_) {
+        o.ptr_ = nullptr;
+        o.bytes_ = 0;
+    }
     void* get() const { return ptr_; }
     size_t size() const { return bytes_; }
 
@@ -105,6 +116,107 @@ std::pair<int64_t, int64_t> factorize(const GridT& grid, const CfgT& cfg) {
     int64_t m = 0, b = 0;
     check(vmb_factorize(&g, &c, &m, &b));
     return {m, b};
+}
+
+// ---------------------------------------------------------------- host <-> device helpers
+template <class MatT>
+DeviceBuffer to_device(const MatT& m) {
+    DeviceBuffer b((size_t)m.rows * m.cols * sizeof(float));
+    if (b.size()) check_cuda(cudaMemcpy(b.get(), m.data.data(), b.size(), cudaMemcpyHostToDevice), "H2D");
+    return b;
+}
+inline DeviceBuffer vec_to_device(const std::vector<float>& v) {
+    DeviceBuffer b(v.size() * sizeof(float));
+    if (b.size()) check_cuda(cudaMemcpy(b.get(), v.data(), b.size(), cudaMemcpyHostToDevice), "H2D");
+    return b;
+}
+template <class MatT>
+MatT mat_from_device(const DeviceBuffer& b, int64_t rows, int64_t cols) {
+    MatT m(rows, cols);
+    if (rows * cols) check_cuda(cudaMemcpy(m.data.data(), b.get(), (size_t)rows * cols * sizeof(float), cudaMemcpyDeviceToHost), "D2H");
+    return m;
+}
+inline std::vector<float> vec_from_device(const DeviceBuffer& b, size_t n) {
+    std::vector<float> v(n);
+    if (n) check_cuda(cudaMemcpy(v.data(), b.get(), n * sizeof(float), cudaMemcpyDeviceToHost), "D2H");
+    return v;
+}
+
+// video.cpp:36-59 (per batch*head unit).  CostT: the caller's CostReport type.
+template <class CostT, class GridT, class CfgT>
+CostT flops_estimate(const GridT& grid, const CfgT& cfg, int64_t d) {
+    const vmb_grid g = to_grid(grid);
+    const vmb_config c = to_config(cfg);
+    CostT r{};
+    uint64_t mf = 0, ff = 0, rf = 0;
+    check(vmb_flops_estimate(&g, &c, d, &r.sparsity, &r.sparsity_approx, &mf, &ff, &rf, &r.reduction_ratio));
+    r.monarch_flops = mf;
+    r.full_attn_flops = ff;
+    r.recompute_flops = rf;
+    return r;
+}
+
+// oracle.hpp:36-72: softmax(Q K^T [/ sqrt d]) V on the device (fp32 parity mode).
+template <class MatT>
+MatT dense_forward(const MatT& q, const MatT& k, const MatT& v, bool scale) {
+    check_dim(q.cols == k.cols && k.cols == v.cols, "Q, K, V must share head dim");
+    check_dim(k.rows == v.rows, "K and V must share row count");
+    check_dim(k.rows >= 1, "attention over empty keys");
+    DeviceBuffer dq = to_device(q), dk = to_device(k), dv = to_device(v), dout((size_t)q.rows * q.cols * sizeof(float));
+    const float qs = scale ? (float)(1.0 / std::sqrt((double)q.cols)) : 1.f;
+    check(vmb_flash_entropy_fwd(1, q.rows, k.rows, q.cols, VMB_F32, dq.get(), dk.get(), dv.get(), qs, dout.get(), nullptr,
+                                nullptr, nullptr));
+    check_cuda(cudaDeviceSynchronize(), "dense_forward");
+    return mat_from_device<MatT>(dout, q.rows, q.cols);
+}
+
+// flash_entropy.hpp:85-139.  ResultT: the caller's FlashFwdResult<float> {output, lse, entropy}.
+template <class ResultT, class MatT, class TileT>
+ResultT flash_entropy_fwd(const MatT& q, const MatT& k, const MatT& v, const TileT& tiles) {
+    check_dim(q.cols == k.cols && k.cols == v.cols, "Q, K, V must share head dim");
+    check_dim(k.rows == v.rows, "K and V must share row count");
+    if (k.rows < 1) throw std::domain_error("domain error: attention over empty keys");
+    check_dim(tiles.b_r >= 1 && tiles.b_c >= 1, "tile sizes must be >= 1");
+    DeviceBuffer dq = to_device(q), dk = to_device(k), dv = to_device(v), dout((size_t)q.rows * q.cols * sizeof(float)),
+                 dl((size_t)q.rows * sizeof(float)), de((size_t)q.rows * sizeof(float));
+    check(vmb_flash_entropy_fwd(1, q.rows, k.rows, q.cols, VMB_F32, dq.get(), dk.get(), dv.get(), 1.f, dout.get(),
+                                (float*)dl.get(), (float*)de.get(), nullptr));
+    check_cuda(cudaDeviceSynchronize(), "flash_entropy_fwd");
+    ResultT r;
+    r.output = mat_from_device<MatT>(dout, q.rows, q.cols);
+    r.lse = vec_from_device(dl, (size_t)q.rows);
+    r.entropy = vec_from_device(de, (size_t)q.rows);
+    return r;
+}
+
+// flash_entropy.hpp:146-221.  ResultT: the caller's FlashBwdResult<float> {dq, dk, dv}.
+template <class ResultT, class MatT, class TileT>
+ResultT flash_entropy_bwd(const MatT& q, const MatT& k, const MatT& v, const MatT& o, const MatT& dout,
+                          const std::vector<float>& lse, const std::vector<float>& entropy,
+                          const std::vector<float>& dentropy, bool entropy_grad, const TileT& tiles) {
+    const int64_t nq = q.rows, nk = k.rows, d = q.cols;
+    check_dim(k.cols == d && v.cols == d && o.cols == d && dout.cols == d, "all operands must share head dim");
+    check_dim(v.rows == nk, "K and V must share row count");
+    check_dim(o.rows == nq && dout.rows == nq, "O and dO must have N_q rows");
+    check_dim((int64_t)lse.size() == nq, "lse length must equal N_q");
+    check_dim(entropy.empty() || (int64_t)entropy.size() == nq, "entropy length must equal N_q");
+    check_dim(dentropy.empty() || (int64_t)dentropy.size() == nq, "dH length must equal N_q");
+    if (entropy_grad) check_dim(!entropy.empty() && !dentropy.empty(), "entropy_grad requires entropy and dH inputs");
+    if (nk < 1) throw std::domain_error("domain error: attention over empty keys");
+    check_dim(tiles.b_r >= 1 && tiles.b_c >= 1, "tile sizes must be >= 1");
+    DeviceBuffer bq = to_device(q), bk = to_device(k), bv = to_device(v), bo = to_device(o), bg = to_device(dout),
+                 bl = vec_to_device(lse), be = vec_to_device(entropy), bd = vec_to_device(dentropy),
+                 gq((size_t)nq * d * sizeof(float)), gk((size_t)nk * d * sizeof(float)), gv((size_t)nk * d * sizeof(float));
+    check(vmb_flash_entropy_bwd(1, nq, nk, d, VMB_F32, bq.get(), bk.get(), bv.get(), bo.get(), bg.get(), (const float*)bl.get(),
+                                entropy.empty() ? nullptr : (const float*)be.get(),
+                                dentropy.empty() ? nullptr : (const float*)bd.get(), entropy_grad ? 1 : 0, gq.get(),
+                                gk.get(), gv.get(), nullptr));
+    check_cuda(cudaDeviceSynchronize(), "flash_entropy_bwd");
+    ResultT r;
+    r.dq = mat_from_device<MatT>(gq, nq, d);
+    r.dk = mat_from_device<MatT>(gk, nk, d);
+    r.dv = mat_from_device<MatT>(gv, nk, d);
+    return r;
 }
 
 // ---------------------------------------------------------------- the operator (video.hpp:84-150)
@@ -175,6 +287,32 @@ std::vector<MatT> vmonarch_attention(std::span<const MatT> qs, std::span<const M
         }
     }
     return out;
+}
+
+// monarch.hpp:155-193 for one (m*b, d) problem: the grid path with T = m, h*w = b and no
+// first-frame recompute.  ResultT: the caller's MonarchResult<float> {output, factors{L, R}};
+// CfgT: MonarchConfig {m, b, iters, clamp_min, clamp_enabled}.
+template <class ResultT, class MatT, class CfgT>
+ResultT monarch_attention(const MatT& q, const MatT& k, const MatT& v, const CfgT& cfg) {
+    const int64_t n = (int64_t)cfg.m * cfg.b;
+    check_dim(q.rows == n && k.rows == n && v.rows == n, "Q, K, V must have m*b rows");
+    check_dim(q.cols == k.cols && k.cols == v.cols, "Q, K, V must share head dim");
+    check_dim(q.cols >= 1, "head dim must be >= 1");
+    struct G { int64_t t_frames, h, w, head_dim, heads, batch; } g{cfg.m, 1, cfg.b, q.cols, 1, 1};
+    struct C {
+        int64_t iters;
+        double clamp_min;
+        bool clamp_enabled, recompute_first_frame;
+        const std::pair<int64_t, int64_t>* override_m_b;
+    } c{cfg.iters, cfg.clamp_min, cfg.clamp_enabled, false, nullptr};
+    std::vector<std::remove_reference_t<decltype(std::declval<ResultT&>().factors)>> f;
+    std::vector<MatT> qs{q}, ks{k}, vs{v};
+    auto out = vmonarch_attention(std::span<const MatT>(qs), std::span<const MatT>(ks), std::span<const MatT>(vs), g, c,
+                                  1, &f);
+    ResultT r;
+    r.output = std::move(out[0]);
+    r.factors = std::move(f[0]);
+    return r;
 }
 
 }  // namespace vmonarch_b200

@@ -15,6 +15,9 @@
 #include <string>
 #include <vector>
 
+#include "vmonarch/flash_entropy.hpp"
+#include "vmonarch/monarch.hpp"
+#include "vmonarch/oracle.hpp"
 #include "vmonarch/video.hpp"
 #include "vmonarch_b200.hpp"
 
@@ -102,6 +105,53 @@ int main() {
     parity_case("clamp disabled, sigma=2", vmonarch::TokenGrid{3, 6, 5, 32, 3, 1}, noclamp, 2.0, false);
     parity_case("batch 2 x heads 2, d=16", vmonarch::TokenGrid{5, 4, 4, 16, 2, 2}, vmonarch::VMonarchConfig{}, 3.0,
                 false);
+
+    // companions: monarch_attention, flash_entropy_fwd / _bwd, dense_forward, flops_estimate
+    {
+        auto q = randn_units(1, 256, 32, 40, 1.0)[0], k = randn_units(1, 256, 32, 41, 1.0)[0],
+             v = randn_units(1, 256, 32, 42, 1.0)[0], g = randn_units(1, 256, 32, 43, 1.0)[0];
+        vmonarch::MonarchConfig mc{16, 16, 3, 0.1, true};
+        auto r1 = vmonarch::monarch_attention(q, k, v, mc);
+        auto r2 = vmonarch_b200::monarch_attention<vmonarch::MonarchResult<float>>(q, k, v, mc);
+        char buf[200];
+        std::snprintf(buf, sizeof buf, "monarch_attention (m,b)=(16,16) t=3: output %.2e, L %.2e, R %.2e",
+                      relfro(r2.output.data, r1.output.data), relfro(r2.factors.L.data, r1.factors.L.data),
+                      relfro(r2.factors.R.data, r1.factors.R.data));
+        expect(relfro(r2.output.data, r1.output.data) <= 1e-4 && relfro(r2.factors.L.data, r1.factors.L.data) <= 1e-4 &&
+                   relfro(r2.factors.R.data, r1.factors.R.data) <= 1e-4, buf);
+        vmonarch::Mat<float> qs = q;
+        for (auto& x : qs.data) x *= 1.f / std::sqrt(32.f);
+        vmonarch::TileConfig tc{16, 32};
+        auto f1 = vmonarch::flash_entropy_fwd(qs, k, v, tc);
+        auto f2 = vmonarch_b200::flash_entropy_fwd<vmonarch::FlashFwdResult<float>>(qs, k, v, tc);
+        const double eo = relfro(f2.output.data, f1.output.data), el = relfro(f2.lse, f1.lse), eh = relfro(f2.entropy, f1.entropy);
+        std::snprintf(buf, sizeof buf, "flash_entropy_fwd: output %.2e, lse %.2e, entropy %.2e", eo, el, eh);
+        expect(eo <= 1e-4 && el <= 1e-5 && eh <= 1e-4, buf);
+        std::vector<float> dh(256);
+        for (int i = 0; i < 256; ++i) dh[i] = 0.01f * (i % 7) - 0.03f;
+        auto b1 = vmonarch::flash_entropy_bwd(qs, k, v, f1.output, g, f1.lse, f1.entropy, dh, true, tc);
+        auto b2 = vmonarch_b200::flash_entropy_bwd<vmonarch::FlashBwdResult<float>>(qs, k, v, f1.output, g, f1.lse,
+                                                                                    f1.entropy, dh, true, tc);
+        const double gq = relfro(b2.dq.data, b1.dq.data), gk = relfro(b2.dk.data, b1.dk.data), gv = relfro(b2.dv.data, b1.dv.data);
+        std::snprintf(buf, sizeof buf, "flash_entropy_bwd (entropy grad): dq %.2e, dk %.2e, dv %.2e", gq, gk, gv);
+        expect(gq <= 1e-4 && gk <= 1e-4 && gv <= 1e-4, buf);
+        auto d1 = vmonarch::dense_forward(q, k, v, true);
+        auto d2 = vmonarch_b200::dense_forward(q, k, v, true);
+        std::snprintf(buf, sizeof buf, "dense_forward: %.2e", relfro(d2.data, d1.data));
+        expect(relfro(d2.data, d1.data) <= 1e-4, buf);
+        vmonarch::TokenGrid wan{81, 28, 52, 64, 1, 1};
+        auto c1 = vmonarch::flops_estimate(wan, vmonarch::VMonarchConfig{}, 64);
+        auto c2 = vmonarch_b200::flops_estimate<vmonarch::CostReport>(wan, vmonarch::VMonarchConfig{}, 64);
+        expect(c1.monarch_flops == c2.monarch_flops && c1.full_attn_flops == c2.full_attn_flops &&
+                   c1.recompute_flops == c2.recompute_flops && c1.reduction_ratio == c2.reduction_ratio &&
+                   c1.sparsity == c2.sparsity,
+               "flops_estimate wan-321f d=64: bit-exact");
+        expect(throws<std::domain_error>([&] {
+                   vmonarch_b200::flash_entropy_fwd<vmonarch::FlashFwdResult<float>>(qs, vmonarch::Mat<float>(0, 32),
+                                                                                     vmonarch::Mat<float>(0, 32), tc);
+               }),
+               "flash over empty keys -> std::domain_error");
+    }
 
     // error contract (check.hpp:10-20): same exception classes as the reference
     auto qs = randn_units(2, 256, 64, 7, 1.0);
