@@ -128,6 +128,32 @@ vmb_status vmb_seq_assemble(const vmb_grid* grid, vmb_dtype dtype, int32_t world
                             const int64_t* pos_count, int64_t slab_max, const void* gathered, void* full,
                             void* stream);
 
+/* ---- single-process multi-GPU ----
+ * One call drives n_dev devices: devices[r] is a CUDA ordinal, streams[r] a stream on it
+ * (streams == NULL: the legacy default streams), and q/k/v/o[r], workspace[r] live on it.
+ * Parts are contiguous and differ in size by at most one (vmb_shard_range).
+ *  VMB_SHARD_HEADS: device r owns the unit block vmb_shard_range(batch*heads, n_dev, r);
+ *    q/k/v/o[r] are (units_r, N, d) contiguous.  Units are independent (video.hpp:115-148),
+ *    so there is no inter-device traffic; results are bitwise equal to the 1-device call.
+ *  VMB_SHARD_SEQ: device r owns spatial positions vmb_shard_range(h*w, n_dev, r) of every
+ *    frame, for every unit: q/k/v/o[r] are (units, T*count_r, d), token t*count_r + i, as in
+ *    vmb_vmonarch_fwd_seq.  The K/V slabs are all-gathered inside the call by one kernel
+ *    per device reading its peers' HBM over NVLink (P2P; peer access is enabled here and
+ *    required, VMB_ERR_NCCL otherwise) into workspace[r]; then the slab forward runs.
+ *    Default factorization; bf16, d = 128, T <= 128.
+ * Stream-ordered on every streams[r]; the call joins all streams (cross-device events)
+ * before the gather and after it, so inputs may be rewritten once streams[r] moves on.
+ * The process-per-GPU equivalent is vmb_vmonarch_fwd_seq + the caller's all-gather
+ * (NCCL) + vmb_seq_assemble. */
+typedef enum { VMB_SHARD_HEADS = 0, VMB_SHARD_SEQ = 1 } vmb_shard_mode;
+void vmb_shard_range(int64_t n, int32_t parts, int32_t r, int64_t* begin, int64_t* count);
+size_t vmb_workspace_size_multi(int32_t n_dev, int32_t rank, vmb_shard_mode mode, const vmb_grid* grid,
+                                const vmb_config* cfg, vmb_dtype dtype);
+vmb_status vmb_vmonarch_fwd_multi(int32_t n_dev, const int32_t* devices, vmb_shard_mode mode, const vmb_grid* grid,
+                                  const vmb_config* cfg, vmb_dtype dtype, const void* const* q, const void* const* k,
+                                  const void* const* v, void* const* o, void* const* workspace,
+                                  const size_t* workspace_bytes, void* const* streams);
+
 /* ---- half steps (monarch.hpp:53-147), unit-major contiguous state tensors ----
  * aR (units,m,b,d) dtype; cR (units,m,b) f32; Kb (units,m,b,d) dtype;
  * aL (units,b,m,d) dtype; cL (units,b,m) f32; Qb (units,b,m,d) dtype (the permuted,

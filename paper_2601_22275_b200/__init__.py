@@ -22,7 +22,7 @@ import ctypes as C
 import math
 import os
 from dataclasses import dataclass, field
-from typing import Optional, Sequence, Tuple
+from typing import List, Optional, Sequence, Tuple
 
 import torch
 
@@ -108,6 +108,11 @@ _vmb_ws_size_seq = _sig("vmb_workspace_size_seq", [C.POINTER(_Grid), C.POINTER(_
 _vmb_fwd_seq = _sig("vmb_vmonarch_fwd_seq", [C.POINTER(_Grid), C.POINTER(_Cfg), C.c_int, _I64, _I64, _P, _P, _P, _P,
                                              _P, C.c_size_t, _P])
 _vmb_seq_assemble = _sig("vmb_seq_assemble", [C.POINTER(_Grid), C.c_int, _I32, _P, _P, _I64, _P, _P, _P])
+_vmb_shard_range = _sig("vmb_shard_range", [_I64, _I32, _I32, C.POINTER(_I64), C.POINTER(_I64)], None)
+_vmb_ws_size_multi = _sig("vmb_workspace_size_multi", [_I32, _I32, C.c_int, C.POINTER(_Grid), C.POINTER(_Cfg),
+                                                       C.c_int], C.c_size_t)
+_vmb_fwd_multi = _sig("vmb_vmonarch_fwd_multi", [_I32, _P, C.c_int, C.POINTER(_Grid), C.POINTER(_Cfg), C.c_int]
+                      + [_P] * 7)
 _vmb_selftest = _sig("vmb_selftest_umma", [_I32, _P, _P, _P, _P])
 
 VMB_F32, VMB_BF16 = 0, 1
@@ -438,6 +443,60 @@ def seq_assemble(gathered: torch.Tensor, grid: TokenGrid, pos_begin: Sequence[in
     _check(_vmb_seq_assemble(C.byref(g), _dtype_code(gathered), world, C.addressof(b), C.addressof(cn), smax,
                              _ptr(gathered.contiguous()), _ptr(out), _stream()))
     return out
+
+
+# ----------------------------------------------------------------------------- single-process multi-GPU
+SHARD_MODES = {"heads": 0, "seq": 1}
+
+
+def shard_range(n: int, parts: int, r: int) -> Tuple[int, int]:
+    """(begin, count) of part r of n items split into `parts` contiguous parts (vmb_shard_range);
+    the same partition as dist.unit_shards / dist.slab_partition."""
+    b, c = _I64(0), _I64(0)
+    _vmb_shard_range(n, parts, r, C.byref(b), C.byref(c))
+    return b.value, c.value
+
+
+def vmonarch_attention_multi(qs: Sequence[torch.Tensor], ks: Sequence[torch.Tensor], vs: Sequence[torch.Tensor],
+                             grid: TokenGrid, cfg: VMonarchConfig = VMonarchConfig(), mode: str = "heads",
+                             check: bool = True) -> List[torch.Tensor]:
+    """One process drives len(qs) GPUs (vmb_vmonarch_fwd_multi).  Part r lives
+    on qs[r].device; mode "heads": (units_r, N, d) unit blocks of shard_range(units, n, r);
+    mode "seq": (units, T*count_r, d) spatial slabs of shard_range(h*w, n, r), with the K/V
+    all-gather done device-to-device over peer memory inside the call.  Returns the per-part
+    outputs, ordered on each device's current stream."""
+    n = len(qs)
+    if not (len(ks) == len(vs) == n) or n == 0:
+        raise DimensionError("dimension error: need one q/k/v tensor per device")
+    _require_cuda(*qs, *ks, *vs)
+    if mode not in SHARD_MODES:
+        raise DimensionError(f"dimension error: unknown shard mode {mode!r}")
+    dt = _dtype_code(qs[0])
+    g, c = grid._c(), cfg._c()
+    qs = [x.contiguous() for x in qs]
+    ks = [x.contiguous() for x in ks]
+    vs = [x.contiguous() for x in vs]
+    outs = [torch.empty_like(x) for x in qs]
+    wss, sizes, streams = [], [], []
+    for r in range(n):
+        nb = int(_vmb_ws_size_multi(n, r, SHARD_MODES[mode], C.byref(g), C.byref(c), dt))
+        if nb == 0:
+            _check(1)
+        wss.append(torch.empty(nb, dtype=torch.uint8, device=qs[r].device))
+        sizes.append(nb)
+        streams.append(torch.cuda.current_stream(qs[r].device).cuda_stream)
+    # the ctypes arrays are kept in locals so they outlive the call
+    pq, pk, pv, po, pw = ((C.c_void_p * n)(*[_ptr(t) for t in ts]) for ts in (qs, ks, vs, outs, wss))
+    devs = (C.c_int32 * n)(*[x.device.index for x in qs])
+    szs = (C.c_size_t * n)(*sizes)
+    sts = (C.c_void_p * n)(*streams)
+    _check(_vmb_fwd_multi(n, C.addressof(devs), SHARD_MODES[mode], C.byref(g), C.byref(c), dt, C.addressof(pq),
+                          C.addressof(pk), C.addressof(pv), C.addressof(po), C.addressof(pw), C.addressof(szs),
+                          C.addressof(sts)))
+    if check:
+        for r in range(n):
+            _check(_vmb_ws_status(_ptr(wss[r]), C.c_void_p(streams[r])))
+    return outs
 
 
 def export_factors(q, k, grid, cfg, dtype_code):

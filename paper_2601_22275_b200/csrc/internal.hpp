@@ -272,6 +272,11 @@ void flash_bwd_launch(int64_t U, int64_t nq, int64_t nk, int64_t d, bool bf16, c
 constexpr int kMaxSeqRanks = 64;
 void seq_assemble(const void* gathered, void* full, int64_t units, int64_t T, int64_t hw, int64_t slab_max,
                   int64_t row_bytes, int world, const int64_t* off, const int64_t* cnt, cudaStream_t s);
+// device-side all-gather over peer memory: slab r of K/V (units, T, cnt[r], d) at k_src[r] /
+// v_src[r] (any device with peer access) -> frame-major (units, T*hw, d) at k_dst / v_dst
+void peer_gather(const void* const* k_src, const void* const* v_src, void* k_dst, void* v_dst, int64_t units,
+                 int64_t T, int64_t hw, int64_t row_bytes, int world, const int64_t* off, const int64_t* cnt,
+                 cudaStream_t s);
 
 void selftest_umma(int mode, const void* A, const void* B, float* C, cudaStream_t s);
 

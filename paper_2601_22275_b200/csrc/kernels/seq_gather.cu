@@ -75,3 +75,90 @@ void seq_assemble(const void* gathered, void* full, int64_t units, int64_t T, in
 }
 
 }  // namespace vmb
+
+// ---------------------------------------------------------------- peer-memory all-gather
+// Single-process multi-GPU sequence-sharded mode (vmb_vmonarch_fwd_multi): device r reads
+// every peer's K and V slab (units, T, cnt_p, d) straight out of the peer's HBM over NVLink
+// (P2P loads through the unified address space) and writes the frame-major (units, N, d)
+// tensors into its own workspace.  One kernel per device replaces the NCCL all-gather plus
+// the assemble pass of the process-per-GPU mode: no padded staging buffer, no second copy.
+namespace vmb {
+namespace {
+
+struct PeerGatherParams {
+    const uint8_t* k_src[kMaxSeqRanks];
+    const uint8_t* v_src[kMaxSeqRanks];
+    uint8_t* k_dst;
+    uint8_t* v_dst;
+    int64_t off[kMaxSeqRanks];
+    int64_t cnt[kMaxSeqRanks];
+    int64_t rows_before[kMaxSeqRanks + 1];  // prefix sum of units * T * cnt_p
+    int64_t units, T, hw, row_bytes;
+    int32_t world;
+};
+
+__global__ void __launch_bounds__(256) peer_gather_kernel(const __grid_constant__ PeerGatherParams p) {
+    const int64_t chunks = p.row_bytes / 16;
+    const int64_t rows = p.rows_before[p.world];
+    const int64_t total = 2 * rows * chunks;  // K then V
+    // consecutive threads take consecutive 16-B chunks of one row, so every warp moves whole
+    // 256-B rows and the peer reads coalesce into full NVLink packets
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = idx % chunks;
+        int64_t row = idx / chunks;
+        const bool is_v = row >= rows;
+        if (is_v) row -= rows;
+        int r = 0;
+        while (row >= p.rows_before[r + 1]) ++r;
+        const int64_t local = row - p.rows_before[r];  // (unit, frame, position) within slab r
+        const int64_t i = local % p.cnt[r];
+        const int64_t ut = local / p.cnt[r];
+        const uint8_t* src = (is_v ? p.v_src[r] : p.k_src[r]) + local * p.row_bytes;
+        uint8_t* dst = (is_v ? p.v_dst : p.k_dst) + (ut * p.hw + p.off[r] + i) * p.row_bytes;
+        reinterpret_cast<uint4*>(dst)[c] = __ldcs(reinterpret_cast<const uint4*>(src) + c);
+    }
+}
+
+}  // namespace
+
+void peer_gather(const void* const* k_src, const void* const* v_src, void* k_dst, void* v_dst, int64_t units,
+                 int64_t T, int64_t hw, int64_t row_bytes, int world, const int64_t* off, const int64_t* cnt,
+                 cudaStream_t s) {
+    VMB_REQUIRE_DIM(world >= 1 && world <= kMaxSeqRanks, "sequence-sharded world size out of range");
+    VMB_REQUIRE_DIM(row_bytes % 16 == 0, "row size must be a multiple of 16 bytes");
+    PeerGatherParams p;
+    p.k_dst = static_cast<uint8_t*>(k_dst);
+    p.v_dst = static_cast<uint8_t*>(v_dst);
+    p.units = units;
+    p.T = T;
+    p.hw = hw;
+    p.row_bytes = row_bytes;
+    p.world = world;
+    p.rows_before[0] = 0;
+    for (int r = 0; r < kMaxSeqRanks; ++r) {
+        const bool in = r < world;
+        p.k_src[r] = in ? static_cast<const uint8_t*>(k_src[r]) : nullptr;
+        p.v_src[r] = in ? static_cast<const uint8_t*>(v_src[r]) : nullptr;
+        p.off[r] = in ? off[r] : 0;
+        p.cnt[r] = in ? cnt[r] : 1;
+        if (in) {
+            VMB_REQUIRE_DIM(cnt[r] >= 1 && off[r] >= 0 && off[r] + cnt[r] <= hw, "slab outside the frame");
+            p.rows_before[r + 1] = p.rows_before[r] + units * T * cnt[r];
+        } else {
+            p.rows_before[r + 1] = p.rows_before[r];
+        }
+    }
+    const int64_t total = 2 * p.rows_before[world] * (row_bytes / 16);
+    if (total == 0) return;
+    int dev = 0, sms = 148;
+    VMB_CHECK_CUDA(cudaGetDevice(&dev));
+    VMB_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8);
+    ProfScope ps(kKSimt, s);
+    peer_gather_kernel<<<(unsigned)blocks, 256, 0, s>>>(p);
+    count_launch();
+    check_launch("peer_gather");
+}
+
+}  // namespace vmb

@@ -766,6 +766,179 @@ vmb_status vmb_seq_assemble(const vmb_grid* grid, vmb_dtype dtype, int32_t world
     });
 }
 
+// ---- single-process multi-GPU (SURVEY §8b vmb_vmonarch_fwd_multi, §8e) ----
+namespace {
+void shard_range(int64_t n, int64_t parts, int64_t r, int64_t& begin, int64_t& count) {
+    const int64_t base = n / parts, extra = n % parts;
+    count = base + (r < extra ? 1 : 0);
+    begin = r * base + std::min(r, extra);
+}
+
+struct DeviceRestore {
+    int prev = 0;
+    DeviceRestore() { cudaGetDevice(&prev); }
+    ~DeviceRestore() { cudaSetDevice(prev); }
+};
+
+// The per-device problem of the multi-GPU call: the unit block (heads) or the spatial slab
+// (seq) of device r, and its workspace layout (seq: the gathered full K and V follow the
+// forward's own workspace).
+struct MultiPart {
+    Shape s;
+    vmb_grid g;
+    int64_t pos_begin = 0, pos_count = 0;
+    size_t fwd_bytes = 0, kv_bytes = 0;
+};
+
+MultiPart multi_part(int32_t n_dev, int32_t r, vmb_shard_mode mode, const vmb_grid* grid, const vmb_config* cfg,
+                     vmb_dtype dt) {
+    VMB_REQUIRE_DIM(grid && cfg, "null grid or config");
+    VMB_REQUIRE_DIM(n_dev >= 1 && n_dev <= kMaxSeqRanks && r >= 0 && r < n_dev, "device count out of range");
+    VMB_REQUIRE_DIM(dt == VMB_F32 || dt == VMB_BF16, "unsupported dtype");
+    MultiPart p;
+    p.g = *grid;
+    if (mode == VMB_SHARD_HEADS) {
+        int64_t u0, uc;
+        shard_range(grid->heads * grid->batch, n_dev, r, u0, uc);
+        p.g.heads = uc;  // a contiguous block of (batch, head) units, unit-major
+        p.g.batch = 1;
+        p.s = make_shape(&p.g, cfg);
+        p.fwd_bytes = carve(nullptr, p.s, dt).bytes;
+    } else if (mode == VMB_SHARD_SEQ) {
+        shard_range(grid->h * grid->w, n_dev, r, p.pos_begin, p.pos_count);
+        p.s = seq_shape(grid, cfg, p.pos_begin, p.pos_count);
+        VMB_REQUIRE_DIM(dt == VMB_BF16 && p.s.d == 128 && p.s.m <= 128,
+                        "the sequence-sharded mode needs bf16, d = 128 and T <= 128");
+        p.fwd_bytes = align_up(carve(nullptr, p.s, dt).bytes);
+        p.kv_bytes = align_up((size_t)p.s.U * p.s.N * p.s.d * (dt == VMB_BF16 ? 2 : 4));
+    } else {
+        VMB_REQUIRE_DIM(false, "unknown shard mode");
+    }
+    return p;
+}
+
+// every stream waits for the work already queued on every other stream (cross-device events)
+void join_streams(int n, const int32_t* dev, const std::vector<cudaStream_t>& st) {
+    std::vector<cudaEvent_t> ev(n);
+    for (int r = 0; r < n; ++r) {
+        VMB_CHECK_CUDA(cudaSetDevice(dev[r]));
+        VMB_CHECK_CUDA(cudaEventCreateWithFlags(&ev[r], cudaEventDisableTiming));
+        VMB_CHECK_CUDA(cudaEventRecord(ev[r], st[r]));
+    }
+    for (int r = 0; r < n; ++r) {
+        VMB_CHECK_CUDA(cudaSetDevice(dev[r]));
+        for (int p = 0; p < n; ++p)
+            if (p != r) VMB_CHECK_CUDA(cudaStreamWaitEvent(st[r], ev[p], 0));
+    }
+    for (int r = 0; r < n; ++r) {
+        VMB_CHECK_CUDA(cudaSetDevice(dev[r]));
+        VMB_CHECK_CUDA(cudaEventDestroy(ev[r]));  // released once the recorded work completes
+    }
+}
+
+void enable_peer_access(int n, const int32_t* dev) {
+    for (int r = 0; r < n; ++r)
+        for (int p = 0; p < n; ++p) {
+            if (dev[r] == dev[p]) continue;
+            int can = 0;
+            VMB_CHECK_CUDA(cudaDeviceCanAccessPeer(&can, dev[r], dev[p]));
+            if (!can)
+                throw Error{VMB_ERR_NCCL, "collective error: no peer access from device " + std::to_string(dev[r]) +
+                                              " to device " + std::to_string(dev[p])};
+            VMB_CHECK_CUDA(cudaSetDevice(dev[r]));
+            const cudaError_t e = cudaDeviceEnablePeerAccess(dev[p], 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled)
+                (void)cudaGetLastError();
+            else
+                VMB_CHECK_CUDA(e);
+        }
+}
+}  // namespace
+
+void vmb_shard_range(int64_t n, int32_t parts, int32_t r, int64_t* begin, int64_t* count) {
+    int64_t b = 0, c = 0;
+    if (parts >= 1 && r >= 0 && r < parts && n >= 0) shard_range(n, parts, r, b, c);
+    if (begin) *begin = b;
+    if (count) *count = c;
+}
+
+size_t vmb_workspace_size_multi(int32_t n_dev, int32_t rank, vmb_shard_mode mode, const vmb_grid* grid,
+                                const vmb_config* cfg, vmb_dtype dtype) {
+    try {
+        const MultiPart p = multi_part(n_dev, rank, mode, grid, cfg, dtype);
+        return p.fwd_bytes + 2 * p.kv_bytes;
+    } catch (const Error& e) {
+        set_error(e.msg);
+        return 0;
+    }
+}
+
+vmb_status vmb_vmonarch_fwd_multi(int32_t n_dev, const int32_t* devices, vmb_shard_mode mode, const vmb_grid* grid,
+                                  const vmb_config* cfg, vmb_dtype dtype, const void* const* q, const void* const* k,
+                                  const void* const* v, void* const* o, void* const* workspace,
+                                  const size_t* ws_bytes, void* const* streams) {
+    return guarded([&] {
+        VMB_REQUIRE_DIM(devices && q && k && v && o && workspace && ws_bytes, "null argument");
+        VMB_REQUIRE_DIM(n_dev >= 1 && n_dev <= kMaxSeqRanks, "device count out of range");
+        DeviceRestore restore;
+        std::vector<MultiPart> parts;
+        std::vector<cudaStream_t> st(n_dev);
+        for (int r = 0; r < n_dev; ++r) {
+            parts.push_back(multi_part(n_dev, r, mode, grid, cfg, dtype));
+            const MultiPart& p = parts.back();
+            VMB_REQUIRE_DIM(workspace[r] != nullptr && ws_bytes[r] >= p.fwd_bytes + 2 * p.kv_bytes,
+                            "workspace too small");
+            VMB_REQUIRE_DIM(p.s.U == 0 || (q[r] && k[r] && v[r] && o[r]), "null tensor pointer");
+            st[r] = streams ? as_stream(streams[r]) : nullptr;
+        }
+        if (mode == VMB_SHARD_HEADS) {
+            // units are independent (video.hpp:115-148): each device runs its block, no traffic
+            for (int r = 0; r < n_dev; ++r) {
+                const MultiPart& p = parts[r];
+                if (p.s.U == 0) continue;
+                VMB_CHECK_CUDA(cudaSetDevice(devices[r]));
+                vmb_strides def;
+                const vmb_strides* io = or_default(nullptr, def, p.s);
+                forward(p.s, *cfg, dtype, q[r], k[r], v[r], o[r], *io, *io, *io, carve(workspace[r], p.s, dtype),
+                        st[r]);
+            }
+            return;
+        }
+        // sequence-sharded: every device gathers all K/V slabs from its peers' memory into
+        // frame-major order, then runs the forward on its own query slab
+        enable_peer_access(n_dev, devices);
+        join_streams(n_dev, devices, st);  // inputs of every device are ready
+        std::vector<int64_t> off(n_dev), cnt(n_dev);
+        for (int r = 0; r < n_dev; ++r) {
+            off[r] = parts[r].pos_begin;
+            cnt[r] = parts[r].pos_count;
+        }
+        const int64_t es = dtype == VMB_BF16 ? 2 : 4;
+        for (int r = 0; r < n_dev; ++r) {
+            const MultiPart& p = parts[r];
+            VMB_CHECK_CUDA(cudaSetDevice(devices[r]));
+            uint8_t* base = static_cast<uint8_t*>(workspace[r]);
+            peer_gather(k, v, base + p.fwd_bytes, base + p.fwd_bytes + p.kv_bytes, p.s.U, p.s.T, p.s.hw,
+                        p.s.d * es, n_dev, off.data(), cnt.data(), st[r]);
+        }
+        join_streams(n_dev, devices, st);  // no device's K/V input is reused before every peer read it
+        for (int r = 0; r < n_dev; ++r) {
+            const MultiPart& p = parts[r];
+            if (p.s.U == 0) continue;
+            VMB_CHECK_CUDA(cudaSetDevice(devices[r]));
+            uint8_t* base = static_cast<uint8_t*>(workspace[r]);
+            vmb_strides local, full;
+            local.token = full.token = p.s.d;
+            local.head = p.s.Nq * p.s.d;
+            local.batch = p.s.H * p.s.Nq * p.s.d;
+            full.head = p.s.N * p.s.d;
+            full.batch = p.s.H * p.s.N * p.s.d;
+            forward(p.s, *cfg, dtype, q[r], base + p.fwd_bytes, base + p.fwd_bytes + p.kv_bytes, o[r], local, full,
+                    local, carve(workspace[r], p.s, dtype), st[r]);
+        }
+    });
+}
+
 vmb_status vmb_workspace_status(void* workspace, void* stream) {
     int32_t flag = 0;
     vmb_status st = guarded([&] {
