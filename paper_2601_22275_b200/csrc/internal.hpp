@@ -196,7 +196,9 @@ void tc2_combine_launch(const Tc2Args& a, cudaStream_t s);
 // fa3_tc.cu: two 128-row query tiles per CTA, ping-pong softmax warpgroups, 128-key tiles
 // (K/V maps with box rows 128).  Same argument block as fa2.
 int tc3_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg, int max_split);
-void tc3_fa_launch(Tc2Args a, int64_t U, cudaStream_t s);
+// returns the launched arguments (nsplit / n_useg set); do_combine = false leaves the split-KV
+// combine to the caller (tc2_combine_launch), e.g. on another stream
+Tc2Args tc3_fa_launch(Tc2Args a, int64_t U, cudaStream_t s, bool do_combine = true);
 // fa5_tc.cu: persistent fa3 (two query tiles per item, ping-pong softmax warpgroups, one CTA
 // per SM over a flattened item stream); same argument block and 128-key K/V boxes.
 int tc5_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg, int max_split);

@@ -477,8 +477,8 @@ int tc3_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg, int max_split
     return nsplit;
 }
 
-void tc3_fa_launch(Tc2Args a, int64_t U, cudaStream_t s) {
-    if (U == 0 || a.q_len == 0) return;
+Tc2Args tc3_fa_launch(Tc2Args a, int64_t U, cudaStream_t s, bool do_combine) {
+    if (U == 0 || a.q_len == 0) return a;
     VMB_REQUIRE_DIM(a.kv_len >= 1, "attention over empty keys");
     VMB_REQUIRE_DIM(!a.cl_out || a.nv == 1, "entropy output needs the key tile as value operand");
     Params p;
@@ -495,7 +495,8 @@ void tc3_fa_launch(Tc2Args a, int64_t U, cudaStream_t s) {
     if (nsplit == 1) p.a.part_o = nullptr;
     if (a.nv == 1) launch<1>(p, n_useg, nsplit, s);
     else launch<2>(p, n_useg, nsplit, s);
-    if (nsplit > 1) tc2_combine_launch(p.a, s);
+    if (nsplit > 1 && do_combine) tc2_combine_launch(p.a, s);
+    return p.a;
 }
 
 }  // namespace vmb

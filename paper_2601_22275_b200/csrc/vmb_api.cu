@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <random>
 #include <vector>
@@ -218,6 +219,40 @@ void attn_launch(const Tc2Args& a, int64_t U, cudaStream_t s, bool rstep, const 
     }
 }
 
+// Overlap of the first-frame recompute with the monarch chain (VMB_OVERLAP=1; off by default:
+// measured 13.57-13.64 vs 13.25-13.53 ms serial at C4 -- the recompute spreads over the whole
+// call and slows every chain kernel by as much as it saves, profiles/r1_fa_variants.md):
+// the chain (R/L half-steps) runs on a high-priority internal stream forked from the caller's
+// stream, the recompute's split-KV partial pass on the caller's stream; the combine joins
+// both.  The block scheduler then hands SMs the recompute leaves idle -- the tails of the
+// attention launches and the HBM-bound L-steps -- to the other stream's kernels.
+struct OverlapStreams {
+    cudaStream_t chain = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+bool overlap_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("VMB_OVERLAP");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+OverlapStreams& overlap_streams() {
+    // per thread and device: fork/join events of concurrent callers never interleave
+    thread_local std::map<int, OverlapStreams> per_dev;
+    int dev = 0;
+    VMB_CHECK_CUDA(cudaGetDevice(&dev));
+    OverlapStreams& o = per_dev[dev];
+    if (!o.chain) {
+        int least = 0, greatest = 0;
+        VMB_CHECK_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        VMB_CHECK_CUDA(cudaStreamCreateWithPriority(&o.chain, cudaStreamNonBlocking, greatest));
+        VMB_CHECK_CUDA(cudaEventCreateWithFlags(&o.fork, cudaEventDisableTiming));
+        VMB_CHECK_CUDA(cudaEventCreateWithFlags(&o.join, cudaEventDisableTiming));
+    }
+    return o;
+}
+
 struct Shape {
     int64_t T, h, w, d, H, B, U, N, m, b, hw;
     bool recompute;
@@ -406,6 +441,17 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
 
     if (tc_eligible(s, dt, in, out, q, k, v, o) && tc_eligible(s, dt, kin, out, q, k, v, o)) {
         // ------------------------------------------------ tcgen05 path
+        const cudaStream_t user_st = st;
+        // overlap only when the recompute goes through split-KV partials: its O rows are then
+        // written by the combine, after the chain's last L-step has written the other rows
+        const bool overlap = recompute && overlap_enabled() && attn_impl(false) == 3 && ws.part_o &&
+                             tc3_plan_splits(s.hwq, s.N, U, kTc2MaxSplit) > 1;
+        OverlapStreams* ov = overlap ? &overlap_streams() : nullptr;
+        if (ov) {
+            VMB_CHECK_CUDA(cudaEventRecord(ov->fork, user_st));
+            VMB_CHECK_CUDA(cudaStreamWaitEvent(ov->chain, ov->fork, 0));
+            st = ov->chain;
+        }
         const CUtensorMap mQrow = user_map(q, in, s, bq, 1, m, bq, 128, 1);    // (d, i, k): query tiles
         const CUtensorMap mK = user_map(k, kin, s, b, 1, m, b, 128, 1);
         const CUtensorMap mV = user_map(v, kin, s, b, 1, m, b, 128, 1);
@@ -532,7 +578,14 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
             f2.part_o = ws.part_o;
             f2.part_lse = ws.part_lse;
             f2.max_split = ws.part_o ? kTc2MaxSplit : 1;
-            attn_launch(f2, U, st, false);
+            if (ov) {
+                const Tc2Args fin = tc3_fa_launch(f2, U, user_st, false);
+                VMB_CHECK_CUDA(cudaEventRecord(ov->join, ov->chain));
+                VMB_CHECK_CUDA(cudaStreamWaitEvent(user_st, ov->join, 0));
+                tc2_combine_launch(fin, user_st);
+            } else {
+                attn_launch(f2, U, st, false);
+            }
         }
         return;
     }
