@@ -121,3 +121,39 @@ def test_cpu_tensors_are_refused(vm):
     x = torch.zeros(2, 256, 64)
     with pytest.raises(vm.DimensionError, match="CUDA"):
         vm.vmonarch_attention(x, x, x, vm.TokenGrid(4, 8, 8, 64, 2, 1))
+
+
+def test_shard_range_and_multi_workspace_sizes(vm):
+    """vmb_shard_range is the partition of dist.unit_shards / slab_partition; the multi-GPU
+    workspace of part r is the forward's workspace for that part (+ the gathered K/V in seq mode)."""
+    import ctypes as C
+    from paper_2601_22275_b200 import _vmb_ws_size_multi, _vmb_ws_size, _vmb_ws_size_seq
+    from paper_2601_22275_b200.dist import slab_partition
+    for n, parts in [(40, 8), (1456, 3), (3, 8)]:
+        assert [vm.shard_range(n, parts, r) for r in range(parts)] == slab_partition(n, parts)
+    assert vm.shard_range(10, 0, 0) == (0, 0)
+    grid = vm.TokenGrid(81, 28, 52, 128, 40, 1)
+    g, c = grid._c(), vm.VMonarchConfig()._c()
+    for r in range(3):
+        u = vm.shard_range(40, 3, r)[1]
+        gp = vm.TokenGrid(81, 28, 52, 128, u, 1)._c()
+        assert _vmb_ws_size_multi(3, r, 0, C.byref(g), C.byref(c), 1) == _vmb_ws_size(C.byref(gp), C.byref(c), 1)
+        cnt = vm.shard_range(28 * 52, 3, r)[1]
+        kv = 40 * grid.tokens() * 128 * 2
+        seq = _vmb_ws_size_multi(3, r, 1, C.byref(g), C.byref(c), 1)
+        assert seq >= _vmb_ws_size_seq(C.byref(g), C.byref(c), 1, cnt) + 2 * kv
+    assert _vmb_ws_size_multi(3, 3, 0, C.byref(g), C.byref(c), 1) == 0        # rank out of range
+    assert _vmb_ws_size_multi(3, 0, 1, C.byref(g), C.byref(c), 0) == 0        # seq mode is bf16-only
+    assert "bf16" in vm._vmb_last_error().decode()
+
+
+def test_torch_op_fake_kernel_on_cpu(vm):
+    """The DiT op's fake kernel (shape propagation) works without a GPU."""
+    import torch
+    from torch._subclasses.fake_tensor import FakeTensorMode
+    import paper_2601_22275_b200.torch_op  # noqa: F401  (registers vmb::vmonarch_attention)
+    with FakeTensorMode():
+        qkv = torch.empty((2, 4 * 8 * 16, 3, 2, 128), dtype=torch.bfloat16)
+        q, k, v = qkv.unbind(2)
+        o = torch.ops.vmb.vmonarch_attention(q, k, v, 4, 8, 16)
+        assert o.shape == (2, 512, 2, 128) and o.dtype == torch.bfloat16
