@@ -535,7 +535,10 @@ def l_update(Qb: torch.Tensor, aL: torch.Tensor, cL: torch.Tensor, want_L: bool 
     _require_cuda(Qb, aL, cL)
     U, b, m, d = Qb.shape
     dt = _dtype_code(Qb)
-    Qb, aL, cL = Qb.contiguous(), aL.contiguous().to(Qb.dtype), cL.contiguous().float()
+    Qb = Qb.contiguous()
+    # aL / cL of None (no r_update yet) reach the ABI as NULL -> StateError, as in the reference
+    aL = aL.contiguous().to(Qb.dtype) if aL is not None else None
+    cL = cL.contiguous().float() if cL is not None else None
     aR = torch.empty((U, m, b, d), dtype=Qb.dtype, device=Qb.device)
     cR = torch.empty((U, m, b), dtype=torch.float32, device=Qb.device)
     L = torch.empty((U, b, m, m), dtype=torch.float32, device=Qb.device) if want_L else None

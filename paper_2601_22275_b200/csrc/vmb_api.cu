@@ -1131,6 +1131,9 @@ vmb_status vmb_lstep(int64_t units, int64_t m, int64_t b, int64_t d, vmb_dtype d
                      const void* aL, const float* cL, void* aR, float* cR, float* L, void* stream) {
     return guarded([&] {
         VMB_REQUIRE_DIM(units >= 0 && m >= 1 && b >= 1 && d >= 1, "factor sizes must be >= 1");
+        // l_update needs the aL / cL of a preceding r_update (check_state, monarch.hpp:111)
+        if (units > 0 && (aL == nullptr || cL == nullptr))
+            throw Error{VMB_ERR_STATE, "state error: l_update called before any r_update"};
         cudaStream_t st = as_stream(stream);
         const bool bf16 = dtype == VMB_BF16;
         const int64_t ud = m * b * d;
