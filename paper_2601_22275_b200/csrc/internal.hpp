@@ -270,6 +270,13 @@ void flash_bwd_launch(int64_t U, int64_t nq, int64_t nk, int64_t d, bool bf16, c
                       const float* dent, int entropy_grad, float* dvec, void* dq, void* dk, void* dv,
                       cudaStream_t s);
 
+// flash_bwd_tc.cu: tcgen05 backward (bf16, d = 128, nq >= 1); rowstat scratch holds
+// flash_bwd_tc_rowstat_rows(nq) float4 per unit
+int64_t flash_bwd_tc_rowstat_rows(int64_t nq);
+void flash_bwd_tc_launch(int64_t U, int64_t nq, int64_t nk, const void* q, const void* k, const void* v,
+                         const void* o, const void* dout, const float* lse, const float* ent, const float* dent,
+                         int entropy_grad, void* rowstat, void* dq, void* dk, void* dv, cudaStream_t s);
+
 // seq_gather.cu: sequence-sharded K/V layout
 constexpr int kMaxSeqRanks = 64;
 void seq_assemble(const void* gathered, void* full, int64_t units, int64_t T, int64_t hw, int64_t slab_max,

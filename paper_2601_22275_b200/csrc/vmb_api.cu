@@ -1255,6 +1255,22 @@ vmb_status vmb_flash_entropy_bwd(int64_t units, int64_t nq, int64_t nk, int64_t 
         VMB_REQUIRE_DIM(units * nq == 0 || (q && o && dout && lse && dq), "null tensor pointer");
         VMB_REQUIRE_DIM(k && v && dk && dv, "null tensor pointer");
         cudaStream_t st = as_stream(stream);
+        // tcgen05 kernels for bf16 / d = 128 (VMB_BWD=simt forces the CUDA-core kernels)
+        static const bool force_simt = [] {
+            const char* e = getenv("VMB_BWD");
+            return e && std::strcmp(e, "simt") == 0;
+        }();
+        auto al32 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31) == 0; };
+        if (!force_simt && dtype == VMB_BF16 && d == 128 && units > 0 && nq > 0 && tmap_supported() &&
+            aligned16(q) && aligned16(k) && aligned16(v) && aligned16(o) && aligned16(dout) && al32(dq) && al32(dk) &&
+            al32(dv)) {
+            void* rowstat = nullptr;
+            const size_t rs_bytes = sizeof(float) * 4 * units * flash_bwd_tc_rowstat_rows(nq);
+            VMB_CHECK_CUDA(cudaMallocAsync(&rowstat, rs_bytes, st));
+            flash_bwd_tc_launch(units, nq, nk, q, k, v, o, dout, lse, ent, dent, entropy_grad, rowstat, dq, dk, dv, st);
+            VMB_CHECK_CUDA(cudaFreeAsync(rowstat, st));
+            return;
+        }
         float* dvec = nullptr;
         if (units * nq > 0) VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dvec), sizeof(float) * units * nq, st));
         flash_bwd_launch(units, nq, nk, d, dtype == VMB_BF16, q, k, v, o, dout, lse, ent, dent, entropy_grad, dvec, dq,
