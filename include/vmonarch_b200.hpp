@@ -133,7 +133,7 @@ inline DeviceBuffer vec_to_device(const std::vector<float>& v) {
 template <class MatT>
 MatT mat_from_device(const DeviceBuffer& b, int64_t rows, int64_t cols) {
     MatT m(rows, cols);
-    if (rows * cols) check_cuda(cudaMemcpy(m.data.data(), b.get(), (size_t)rows * cols * sizeof(float), cudaMemcpyDeviceToHost), "D2H");
+    if (rows * cols > 0) check_cuda(cudaMemcpy(m.data.data(), b.get(), (size_t)rows * cols * sizeof(float), cudaMemcpyDeviceToHost), "D2H");
     return m;
 }
 inline std::vector<float> vec_from_device(const DeviceBuffer& b, size_t n) {
