@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
     using SM = Smem<NB, NO>;
     constexpr int S = SM::S;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::bar_off);
     uint64_t* q_full = bars;
     uint64_t* kv_full = bars + 1;

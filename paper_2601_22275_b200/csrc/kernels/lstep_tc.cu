@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
     const int R = p.rows;
     const Layout L(R, FINAL);
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
     uint64_t* bar_load = reinterpret_cast<uint64_t*>(smem + L.bars);
     uint64_t* bar_mma1 = bar_load + 1;
     uint64_t* bar_mma2 = bar_load + 2;
@@ -191,15 +191,20 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
 
     if (!FINAL && t < m) {
         // cR[k,i] = sum_j L[j,k]  (monarch.hpp:139-143), k = t, from the bf16 copy of L
-        float col0 = 0.f, col1 = 0.f;
+        // 8 independent chains: the loads of a group issue back to back instead of one
+        // shared-memory latency per row
+        float col[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         const uint8_t* base = smem + L.al + (t >> 6) * L.panel;
+        auto lj = [&](int j) {
+            return __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(base + sw128_offset(j, t & 63)));
+        };
         int j = 0;
-        for (; j + 1 < m; j += 2) {
-            col0 += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(base + sw128_offset(j, t & 63)));
-            col1 += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(base + sw128_offset(j + 1, t & 63)));
+        for (; j + 8 <= m; j += 8) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) col[e] += lj(j + e);
         }
-        if (j < m) col0 += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(base + sw128_offset(j, t & 63)));
-        a.cR[((int64_t)u * m + t) * a.b + i] = col0 + col1;
+        for (; j < m; ++j) col[j & 7] += lj(j);
+        a.cR[((int64_t)u * m + t) * a.b + i] = ((col[0] + col[1]) + (col[2] + col[3])) + ((col[4] + col[5]) + (col[6] + col[7]));
     }
 
     // ---- epilogue: TMEM row t -> bf16 SW128 staging tile over Qb -> TMA store

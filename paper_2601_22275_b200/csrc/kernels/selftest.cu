@@ -25,7 +25,7 @@ struct Params {
 
 __global__ void __launch_bounds__(128) selftest_kernel(const __grid_constant__ Params p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
     uint8_t* sA = smem;
     uint8_t* sB = smem + 2 * kPanel;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 4 * kPanel);
