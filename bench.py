@@ -78,7 +78,15 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
-    def stop(self):
+    def ready(self, timeout: float = 5.0) -> int:
+        """Wait until nvidia-smi delivers its first sample (its start-up can outlast a short
+        timed region); returns the index the timed region's samples start from."""
+        t0 = time.time()
+        while self.proc and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.02)
+        return len(self.lines)
+
+    def stop(self, since: int = 0):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
         self.proc.terminate()
@@ -88,7 +96,9 @@ class ClockSampler:
             self.proc.kill()
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        # samples taken while the timed region ran (the one just before it if none landed inside)
+        window = self.lines[since:] or self.lines[max(0, since - 1):since]
+        for ln in window:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -282,7 +292,7 @@ def main():
     barrier()
     torch.cuda.synchronize()
     sampler.start()
-    time.sleep(0.15)
+    since = sampler.ready()
     launches0 = vm.kernel_launch_count()
     prof_enable(1)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -293,7 +303,7 @@ def main():
     torch.cuda.synchronize()
     prof_enable(0)
     launches = vm.kernel_launch_count() - launches0
-    clocks = sampler.stop()
+    clocks = sampler.stop(since)
     barrier()
     ms_local = e0.elapsed_time(e1) / args.steps
     ms = max_over_ranks(ms_local)
