@@ -473,17 +473,17 @@ int tc3_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg, int max_split
     // ~8 waves of one CTA per SM, at least 8 key tiles per split
     const int64_t base = ((q_len + 2 * kQTile - 1) / (2 * kQTile)) * n_useg;
     const int64_t want = (8 * 148 + base - 1) / base;
-    const int64_t hi = std::min<int64_t>({2 * want, (int64_t)max_split, total_tiles / 8});
-    int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(want, hi));
-    // one CTA per SM and equal CTAs: pick the split count (up to 2x the ~8-wave target) whose
-    // last wave is fullest (C4: 240 tile pairs x 5 splits = 8.11 waves wastes 10% of the
-    // ninth; x 8 = 12.97 waves)
-    double best = -1.0;
-    for (int64_t sp = nsplit; sp <= hi; ++sp) {
-        const double waves = (double)(base * sp) / 148.0;
-        const double eff = waves / std::ceil(waves);
-        if (eff > best + 1e-3) {
-            best = eff;
+    const int64_t hi = std::max<int64_t>(1, std::min<int64_t>({2 * want, (int64_t)max_split, total_tiles / 8}));
+    // one CTA per SM and equal CTAs: the call takes ceil(base * s / 148) waves of 1/s of a row
+    // each; minimise that (plus 0.5% per split for the partials and the combine).  C4: 240 tile
+    // pairs -> 8 splits (12.97 waves) instead of 5 (8.11 waves, a nearly empty ninth); 5 heads
+    // per GPU: 30 pairs -> 14 splits (2.84 waves) instead of 16 (3.24)
+    int nsplit = 1;
+    double best = 1e30;
+    for (int64_t sp = 1; sp <= hi; ++sp) {
+        const double t = std::ceil((double)(base * sp) / 148.0) / (double)sp * (1.0 + 0.005 * (double)sp);
+        if (t < best - 1e-9) {
+            best = t;
             nsplit = (int)sp;
         }
     }
