@@ -199,6 +199,8 @@ int tc3_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg, int max_split
 // returns the launched arguments (nsplit / n_useg set); do_combine = false leaves the split-KV
 // combine to the caller (tc2_combine_launch), e.g. on another stream
 Tc2Args tc3_fa_launch(Tc2Args a, int64_t U, cudaStream_t s, bool do_combine = true);
+// fa6_tc.cu: fa3's CTA with 64-key double-buffered score tiles per query tile (A/B variant)
+Tc2Args tc6_fa_launch(Tc2Args a, int64_t U, cudaStream_t s, bool do_combine = true);
 // fa5_tc.cu: persistent fa3 (two query tiles per item, ping-pong softmax warpgroups, one CTA
 // per SM over a flattened item stream); same argument block and 128-key K/V boxes.
 int tc5_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg, int max_split);

@@ -131,12 +131,12 @@ int attn_impl(bool rstep) {
     static const int r = [] {
         const char* e = getenv("VMB_RSTEP");
         const int v = e ? atoi(e) : 2;
-        return (v == 1 || v == 4 || v == 5) ? v : 2;
+        return (v == 1 || v == 4 || v == 5 || v == 6) ? v : 2;
     }();
     static const int at = [] {
         const char* e = getenv("VMB_ATTN");
         const int v = e ? atoi(e) : 3;
-        return (v == 2 || v == 4 || v == 5) ? v : 3;
+        return (v == 2 || v == 4 || v == 5 || v == 6) ? v : 3;
     }();
     return rstep ? r : at;
 }
@@ -146,13 +146,16 @@ namespace {
 constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
 // key-tile rows of the attention kernel family in use (the K/V TMA box height)
-uint32_t attn_kv_box(bool rstep) { return attn_impl(rstep) == 2 ? (uint32_t)tc2_kv_tile(1) : 128u; }
+uint32_t attn_kv_box(bool rstep) {
+    const int impl = attn_impl(rstep);
+    return impl == 2 ? (uint32_t)tc2_kv_tile(1) : impl == 6 ? 64u : 128u;
+}
 int attn_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg) {
     switch (attn_impl(false)) {
         case 2: return tc2_plan_splits(q_len, kv_len, n_useg, 2, kTc2MaxSplit);
         case 4: return tc4_plan_splits(q_len, kv_len, n_useg, kTc2MaxSplit);
         case 5: return tc5_plan_splits(q_len, kv_len, n_useg, kTc2MaxSplit);
-        default: return tc3_plan_splits(q_len, kv_len, n_useg, kTc2MaxSplit);
+        default: return tc3_plan_splits(q_len, kv_len, n_useg, kTc2MaxSplit);  // fa3 and fa6
     }
 }
 // query rows for fa4's entropy dot: row (u, s, r) at base + (u/Hn)*B + (u%Hn)*H + s*S + r*R
@@ -200,6 +203,7 @@ void attn_launch(const Tc2Args& a, int64_t U, cudaStream_t s, bool rstep, const 
         case 2: tc2_fa_launch(a, U, s); break;
         case 4: tc4_fa_launch(to_tc4(a, qv), U, s); break;
         case 5: tc5_fa_launch(a, U, s); break;
+        case 6: tc6_fa_launch(a, U, s); break;
         case 1:  // original 1-CTA/SM kernel (R half-step only)
         default:
             if (rstep && attn_impl(true) == 1) {

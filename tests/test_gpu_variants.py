@@ -38,7 +38,7 @@ print(json.dumps(res))
 
 @pytest.mark.parametrize("env", [{"VMB_RSTEP": "1"}, {"VMB_RSTEP": "4"}, {"VMB_RSTEP": "5"}, {"VMB_ATTN": "2"},
                                  {"VMB_ATTN": "4"}, {"VMB_ATTN": "5"}, {"VMB_RSTEP": "1", "VMB_FA_MC": "1"},
-                                 {"VMB_LSTEP": "2"}],
+                                 {"VMB_LSTEP": "2"}, {"VMB_ATTN": "6"}, {"VMB_RSTEP": "6"}],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_kernel_family_parity(cuda, env):
     r = subprocess.run([sys.executable, "-c", SCRIPT % {"root": ROOT}], capture_output=True, text=True,
