@@ -276,6 +276,13 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def sum_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
     # ---- device-resident timed region
     step(check=True)   # validates once (raises on error)
     for _ in range(args.warmup):
@@ -367,20 +374,19 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.e2e_steps)
+        # whole-job bytes: every rank copies its own heads in and out
         e2e = {"value": round(e2e_ms, 3), "unit": "ms/call",
-               "h2d_bytes_per_step": 3 * q.numel() * q.element_size(),
-               "d2h_bytes_per_step": o.numel() * o.element_size(),
+               "h2d_bytes_per_step": int(sum_over_ranks(3 * q.numel() * q.element_size())),
+               "d2h_bytes_per_step": int(sum_over_ranks(o.numel() * o.element_size())),
                "path": (f"vmonarch_attention_host: pinned host Q/K/V -> HBM -> libvmb forward -> pinned host O, "
                         f"{args.e2e_chunk} heads per chunk pipelined over 3 CUDA streams")}
 
     # ---- dense FlashAttention-style bf16 baseline on the same GPU (same heads)
     dense = None
     if not args.no_dense and args.shard == "heads" and args.config != "c5":
-        od = torch.empty_like(q)
-        vm.dense_forward(q[:1], k[:1], v[:1])
+        vm.dense_forward(q[:1], k[:1], v[:1])  # warm-up (kernel attributes, tensor maps)
         torch.cuda.synchronize()
         e0.record()
-        vm.lib.vmb_dense_fwd  # noqa
         od = vm.dense_forward(q, k, v)
         e1.record()
         torch.cuda.synchronize()
