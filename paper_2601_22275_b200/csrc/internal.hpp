@@ -263,6 +263,21 @@ struct TcLstepArgs {
     float out_scale;    // multiplies the epilogue (ITER: aR scale)
 };
 void tc_lstep_launch(const TcLstepArgs& a, int64_t U, cudaStream_t s);
+// lstep_big.cu: L half-step / apply for m > 128 (row statistics pass + ITER or FINAL pass)
+struct TcLstepBigArgs {
+    CUtensorMap tmQ128, tmQ64;    // Qb rows (d, i, j, head, batch), boxes (64, 1, 128) / (64, 1, 64)
+    CUtensorMap tmAL128, tmAL64;  // aL rows (d, k, i, 1, unit), boxes (64, 128, 1) / (64, 64, 1)
+    CUtensorMap tmY64;            // FINAL: y rows (d, i, k, 1, unit), box (64, 1, 64)
+    const float* cL;              // (U, b, m)
+    float* lse2;                  // (U, b, m) scratch: base-2 row log-sum-exp of S
+    float* cR;                    // ITER: (U, m, b)
+    __nv_bfloat16* aR;            // ITER: (U, m, b, d)
+    __nv_bfloat16* out;           // FINAL: O, row j*b + i of unit (ob, oh) at ob*oB + oh*oH + row*oT
+    int64_t oB, oH, oT;
+    float qscale, out_scale;
+    int32_t m, b, H, oHn;
+};
+void tc_lstep_big_launch(const TcLstepBigArgs& a, int64_t U, bool final_mode, cudaStream_t s);
 // lstep_p.cu: persistent, pipelined variant (producer warp + TMA ring, two consumer warpgroups)
 void tc_lstep_p_launch(const TcLstepArgs& a, int64_t U, cudaStream_t s);
 

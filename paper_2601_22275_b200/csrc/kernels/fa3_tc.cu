@@ -35,6 +35,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "../internal.hpp"
 #include "sm100_ptx.cuh"
@@ -469,24 +470,20 @@ void launch(const Params& p, int64_t n_useg, int nsplit, cudaStream_t s) {
 
 int tc3_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg, int max_split) {
     if (max_split <= 1 || q_len <= 0 || n_useg <= 0) return 1;
+    static const int forced = [] {  // A/B measurement only
+        const char* e = getenv("VMB_SPLITS");
+        return e ? atoi(e) : 0;
+    }();
+    if (forced > 0) return std::min(forced, max_split);
     const int64_t total_tiles = (kv_len + kBN - 1) / kBN;
-    // ~8 waves of one CTA per SM, at least 8 key tiles per split
-    const int64_t base = ((q_len + 2 * kQTile - 1) / (2 * kQTile)) * n_useg;
-    const int64_t want = (8 * 148 + base - 1) / base;
-    const int64_t hi = std::max<int64_t>(1, std::min<int64_t>({2 * want, (int64_t)max_split, total_tiles / 8}));
-    // one CTA per SM and equal CTAs: the call takes ceil(base * s / 148) waves of 1/s of a row
-    // each; minimise that (plus 0.5% per split for the partials and the combine).  C4: 240 tile
-    // pairs -> 8 splits (12.97 waves) instead of 5 (8.11 waves, a nearly empty ninth); 5 heads
-    // per GPU: 30 pairs -> 14 splits (2.84 waves) instead of 16 (3.24)
-    int nsplit = 1;
-    double best = 1e30;
-    for (int64_t sp = 1; sp <= hi; ++sp) {
-        const double t = std::ceil((double)(base * sp) / 148.0) / (double)sp * (1.0 + 0.005 * (double)sp);
-        if (t < best - 1e-9) {
-            best = t;
-            nsplit = (int)sp;
-        }
-    }
+    // The split count depends on the per-unit shape only, never on the number of units in
+    // the call: a unit's output is then bitwise the same whether it runs alone, in a batch or
+    // on another GPU of a head-sharded job (test_video.cpp:197-216).  ~84 CTAs per unit
+    // (C4: 6 tile pairs x 14 splits) keep 5-heads-per-GPU loads at 2.84 waves and cost ~1% at
+    // 40 heads against the best per-U choice (profiles/r1_fa_variants.md).
+    const int64_t pairs = (q_len + 2 * kQTile - 1) / (2 * kQTile);
+    const int64_t cap = std::max<int64_t>(1, std::min<int64_t>({(int64_t)max_split, 14, total_tiles / 8}));
+    int nsplit = (int)std::min<int64_t>(cap, (84 + pairs - 1) / pairs);
     while (nsplit > 1 && ((total_tiles + nsplit - 1) / nsplit) * (nsplit - 1) >= total_tiles) --nsplit;
     return nsplit;
 }

@@ -306,6 +306,7 @@ struct Workspace {
     float* cL;
     float* part_o;    // split-KV partials of the first-frame recompute (tcgen05 path)
     float* part_lse;
+    float* lse2;      // m > 128 (lstep_big.cu): row log-sum-exp of the L-step scores, (U, b, m)
     int nsplit;
     size_t bytes;
 };
@@ -324,6 +325,11 @@ Workspace carve(void* base, const Shape& s, vmb_dtype dt) {
     w.cR = reinterpret_cast<float*>(p + off); off += st;
     w.cL = reinterpret_cast<float*>(p + off); off += st;
     w.part_o = w.part_lse = nullptr;
+    w.lse2 = nullptr;
+    if (s.m > 128) {
+        w.lse2 = reinterpret_cast<float*>(p + off);
+        off += st;
+    }
     w.nsplit = 1;
     if (dt == VMB_BF16 && s.d == 128 && s.recompute && s.U > 0) {
         w.nsplit = attn_plan_splits(s.hwq, s.N, s.U);
@@ -402,8 +408,10 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 
 bool tc_eligible(const Shape& s, vmb_dtype dt, const vmb_strides& in, const vmb_strides& out,
                  const void* q, const void* k, const void* v, const void* o) {
-    if (dt != VMB_BF16 || s.d != 128 || s.m > 128 || !tmap_supported()) return false;
+    if (dt != VMB_BF16 || s.d != 128 || !tmap_supported()) return false;
     if (s.N > (int64_t)INT32_MAX || s.b > 65535 * 16) return false;
+    // the R-step grids put (unit, frame block) on grid.y
+    if (s.U * s.m > 65535) return false;
     const int64_t strides[6] = {in.batch, in.head, in.token, out.batch, out.head, out.token};
     for (int64_t x : strides)
         if (x % 8 != 0) return false;
@@ -460,7 +468,8 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
         const CUtensorMap mK = user_map(k, kin, s, b, 1, m, b, 128, 1);
         const CUtensorMap mV = user_map(v, kin, s, b, 1, m, b, 128, 1);
         const CUtensorMap mK2 = user_map(k, kin, s, b, 1, m, b, attn_kv_box(true), 1);  // attention key tiles
-        const uint32_t lrows = (uint32_t)lstep_rows(m);
+        // (the lstep_tc boxes; with m > 128 the multi-pass L-step builds its own maps)
+        const uint32_t lrows = (uint32_t)std::min<int64_t>(lstep_rows(m), 128);
         const CUtensorMap mQcol = user_map(q, in, s, bq, 1, m, bq, 1, lrows);   // (d, i, j): Qb[i] boxes
         const CUtensorMap mAR = internal_map(ws.aR, U, m, bq, d, true, 128, 1);  // aR (U,m,bq,d): (d,i,k) query tiles
         const CUtensorMap mARst = internal_map(ws.aR, U, m, bq, d, true, 1, lrows);  // aR columns (d,i,k), L-step store
@@ -559,8 +568,34 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
                 const char* e = getenv("VMB_LSTEP");
                 return e && e[0] == '2';
             }();
-            if (lstep_pipelined) tc_lstep_p_launch(ls, U, st);
-            else tc_lstep_launch(ls, U, st);
+            if (m > 128) {
+                // more than 128 row blocks (general factorizations): multi-pass L-step
+                TcLstepBigArgs lb{};
+                lb.tmQ128 = user_map(q, in, s, bq, 1, m, bq, 1, 128);
+                lb.tmQ64 = user_map(q, in, s, bq, 1, m, bq, 1, 64);
+                lb.tmAL128 = internal_map(ws.aL, U, bq, m, d, true, 128, 1);
+                lb.tmAL64 = internal_map(ws.aL, U, bq, m, d, true, 64, 1);
+                lb.tmY64 = internal_map(ws.y, U, m, bq, d, true, 1, 64);
+                lb.cL = ws.cL;
+                lb.lse2 = ws.lse2;
+                lb.cR = ws.cR;
+                lb.aR = static_cast<__nv_bfloat16*>(ws.aR);
+                lb.out = static_cast<__nv_bfloat16*>(o);
+                lb.oB = out.batch;
+                lb.oH = out.head;
+                lb.oT = out.token;
+                lb.qscale = qscale;
+                lb.out_scale = last ? 1.f : qscale;
+                lb.m = (int32_t)m;
+                lb.b = (int32_t)bq;
+                lb.H = (int32_t)std::max<int64_t>(s.H, 1);
+                lb.oHn = (int32_t)std::max<int64_t>(s.H, 1);
+                tc_lstep_big_launch(lb, U, last, st);
+            } else if (lstep_pipelined) {
+                tc_lstep_p_launch(ls, U, st);
+            } else {
+                tc_lstep_launch(ls, U, st);
+            }
         }
         if (recompute) {
             // first-frame recompute: Q[0:hw) against all N keys, split over the keys

