@@ -294,6 +294,12 @@ void flash_bwd_tc_launch(int64_t U, int64_t nq, int64_t nk, const void* q, const
                          const void* o, const void* dout, const float* lse, const float* ent, const float* dent,
                          int entropy_grad, void* rowstat, void* dq, void* dk, void* dv, cudaStream_t s);
 
+// seq_gather.cu: head-dim padding for d < 128 on the tcgen05 path.  to_padded: user rows
+// (unit u = b*H + h at b*sb + h*sh + n*st elements, d columns) -> contiguous (U, N, 128) with
+// zero columns [d, 128); otherwise the reverse (first d columns back to the user layout).
+void pad_rows(const void* src, void* dst, int64_t U, int64_t N, int64_t d, int64_t H, int64_t sb, int64_t sh,
+              int64_t st, bool to_padded, cudaStream_t s);
+
 // seq_gather.cu: sequence-sharded K/V layout
 constexpr int kMaxSeqRanks = 64;
 void seq_assemble(const void* gathered, void* full, int64_t units, int64_t T, int64_t hw, int64_t slab_max,

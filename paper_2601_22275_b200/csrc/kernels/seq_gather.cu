@@ -162,3 +162,69 @@ void peer_gather(const void* const* k_src, const void* const* v_src, void* k_dst
 }
 
 }  // namespace vmb
+
+// ---------------------------------------------------------------- head-dim padding (d < 128)
+namespace vmb {
+namespace {
+
+__global__ void __launch_bounds__(256) pad_rows_kernel(const uint8_t* src, uint8_t* dst, int64_t U, int64_t N,
+                                                       int64_t chunks_real, int64_t H, int64_t sb, int64_t sh,
+                                                       int64_t st, int to_padded) {
+    // one 16-byte chunk per thread; a padded row is 16 chunks (128 bf16)
+    const int64_t total = U * N * 16;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = idx & 15, row = idx >> 4;
+        const int64_t u = row / N, n = row % N;
+        const int64_t user = ((u / H) * sb + (u % H) * sh + n * st) * 2;  // bytes
+        if (to_padded) {
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (c < chunks_real) v = reinterpret_cast<const uint4*>(src + user)[c];
+            reinterpret_cast<uint4*>(dst + row * 256)[c] = v;
+        } else if (c < chunks_real) {
+            reinterpret_cast<uint4*>(dst + user)[c] = reinterpret_cast<const uint4*>(src + row * 256)[c];
+        }
+    }
+}
+
+// element-wise variant for user tensors whose rows are not 16-byte aligned
+__global__ void __launch_bounds__(256) pad_rows_any_kernel(const uint16_t* src, uint16_t* dst, int64_t U, int64_t N,
+                                                           int64_t d, int64_t H, int64_t sb, int64_t sh, int64_t st,
+                                                           int to_padded) {
+    const int64_t total = U * N * 128;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t x = idx & 127, row = idx >> 7;
+        const int64_t u = row / N, n = row % N;
+        const int64_t user = (u / H) * sb + (u % H) * sh + n * st;
+        if (to_padded) dst[idx] = x < d ? src[user + x] : (uint16_t)0;
+        else if (x < d) dst[user + x] = src[idx];
+    }
+}
+
+}  // namespace
+
+void pad_rows(const void* src, void* dst, int64_t U, int64_t N, int64_t d, int64_t H, int64_t sb, int64_t sh,
+              int64_t st, bool to_padded, cudaStream_t s) {
+    if (U * N == 0) return;
+    const void* user = to_padded ? src : dst;
+    const bool vec = (reinterpret_cast<uintptr_t>(user) & 15) == 0 && d % 8 == 0 && sb % 8 == 0 && sh % 8 == 0 &&
+                     st % 8 == 0;
+    const int64_t total = U * N * (vec ? 16 : 128);
+    int dev = 0, sms = 148;
+    VMB_CHECK_CUDA(cudaGetDevice(&dev));
+    VMB_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sms * 16);
+    ProfScope ps(kKSimt, s);
+    if (vec)
+        pad_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst),
+                                                         U, N, d / 8, H, sb, sh, st, to_padded ? 1 : 0);
+    else
+        pad_rows_any_kernel<<<(unsigned)blocks, 256, 0, s>>>(static_cast<const uint16_t*>(src),
+                                                             static_cast<uint16_t*>(dst), U, N, d, H, sb, sh, st,
+                                                             to_padded ? 1 : 0);
+    count_launch();
+    check_launch("pad_rows");
+}
+
+}  // namespace vmb

@@ -263,6 +263,9 @@ struct Shape {
     // query-side extent: all b positions (bq == b, Nq == N, hwq == hw) or, in the
     // sequence-sharded mode, a slab of bq spatial positions of every frame
     int64_t bq = 0, Nq = 0, hwq = 0;
+    // head dim of the caller's tensors when they were zero-padded to d = 128 for the tcgen05
+    // kernels (0: not padded); it sets the softmax scale 1/sqrt(d) (video.hpp:64-78)
+    int64_t d_real = 0;
 };
 
 Shape make_shape(const vmb_grid* g, const vmb_config* c) {
@@ -443,7 +446,7 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
              const void* v, void* o, const vmb_strides& in, const vmb_strides& kin, const vmb_strides& out,
              const Workspace& ws, cudaStream_t st) {
     const bool bf16 = dt == VMB_BF16;
-    const float qscale = (float)(1.0 / std::sqrt((double)s.d));
+    const float qscale = (float)(1.0 / std::sqrt((double)(s.d_real > 0 ? s.d_real : s.d)));
     const bool recompute = cfg.recompute_first_frame != 0;
     const bool skip_j0 = recompute && s.b == s.hw;
     const int64_t U = s.U, m = s.m, b = s.b, d = s.d, bq = s.bq;
@@ -706,6 +709,20 @@ const vmb_strides* or_default(const vmb_strides* s, vmb_strides& tmp, const Shap
     return &tmp;
 }
 int64_t ceil16(int64_t x) { return (x + 15) & ~int64_t(15); }
+
+// Head dims below 128 (the reference default is 64, video.hpp:20) run on the tcgen05 kernels
+// with Q, K, V zero-padded to 128 columns in the workspace: zero columns add nothing to any
+// score or product, so every half-step is exact, and the padded output columns are dropped.
+bool padded_path(const Shape& s, vmb_dtype dt) {
+    return dt == VMB_BF16 && s.d < 128 && tmap_supported() && s.U * s.m <= 65535 && s.N <= (int64_t)INT32_MAX;
+}
+Shape padded_shape(const Shape& s) {
+    Shape p = s;
+    p.d_real = s.d;
+    p.d = 128;
+    return p;
+}
+size_t padded_tensor_bytes(const Shape& s) { return align_up((size_t)s.U * s.N * 128 * 2); }
 }  // namespace
 
 extern "C" {
@@ -777,6 +794,10 @@ vmb_status vmb_flops_estimate(const vmb_grid* grid, const vmb_config* cfg, int64
 size_t vmb_workspace_size(const vmb_grid* grid, const vmb_config* cfg, vmb_dtype dtype) {
     try {
         const Shape s = make_shape(grid, cfg);
+        if (padded_path(s, dtype)) {
+            const Shape p = padded_shape(s);
+            return align_up(carve(nullptr, p, dtype).bytes) + 4 * padded_tensor_bytes(p);
+        }
         return carve(nullptr, s, dtype).bytes;
     } catch (const Error& e) {
         set_error(e.msg);
@@ -794,6 +815,26 @@ vmb_status vmb_vmonarch_fwd(const vmb_grid* grid, const vmb_config* cfg, vmb_dty
         const vmb_strides* in = or_default(in_strides, ti, s);
         const vmb_strides* out = or_default(out_strides, to, s);
         VMB_REQUIRE_DIM(in->token >= s.d && out->token >= s.d, "token stride must be >= head dim");
+        if (padded_path(s, dtype)) {
+            const Shape p = padded_shape(s);
+            const size_t fwd_bytes = align_up(carve(nullptr, p, dtype).bytes), tb = padded_tensor_bytes(p);
+            VMB_REQUIRE_DIM(workspace != nullptr && ws_bytes >= fwd_bytes + 4 * tb, "workspace too small");
+            VMB_REQUIRE_DIM(s.U == 0 || (q && k && v && o), "null tensor pointer");
+            uint8_t* base = static_cast<uint8_t*>(workspace);
+            void* pq = base + fwd_bytes;
+            void* pk = base + fwd_bytes + tb;
+            void* pv = base + fwd_bytes + 2 * tb;
+            void* po = base + fwd_bytes + 3 * tb;
+            cudaStream_t st = as_stream(stream);
+            const int64_t H = std::max<int64_t>(s.H, 1);
+            pad_rows(q, pq, s.U, s.N, s.d, H, in->batch, in->head, in->token, true, st);
+            pad_rows(k, pk, s.U, s.N, s.d, H, in->batch, in->head, in->token, true, st);
+            pad_rows(v, pv, s.U, s.N, s.d, H, in->batch, in->head, in->token, true, st);
+            const vmb_strides dp = default_strides(p);
+            forward(p, *cfg, dtype, pq, pk, pv, po, dp, dp, dp, carve(workspace, p, dtype), st);
+            pad_rows(po, o, s.U, s.N, s.d, H, out->batch, out->head, out->token, false, st);
+            return;
+        }
         const Workspace ws = carve(workspace, s, dtype);
         VMB_REQUIRE_DIM(workspace != nullptr && ws_bytes >= ws.bytes, "workspace too small");
         VMB_REQUIRE_DIM(s.U == 0 || (q && k && v && o), "null tensor pointer");
@@ -1055,14 +1096,24 @@ vmb_status vmb_export_factors(const vmb_grid* grid, const vmb_config* cfg, vmb_d
                               const void* k, const vmb_strides* in_strides, void* workspace, float* L, float* R,
                               void* stream) {
     return guarded([&] {
-        const Shape s = make_shape(grid, cfg);
+        Shape s = make_shape(grid, cfg);
         vmb_strides ti;
         const vmb_strides* in = or_default(in_strides, ti, s);
+        const float qscale = (float)(1.0 / std::sqrt((double)s.d));
+        if (padded_path(s, dtype)) {
+            // the forward ran on the zero-padded copies it left in the workspace
+            const Shape p = padded_shape(s);
+            const size_t fwd_bytes = align_up(carve(nullptr, p, dtype).bytes), tb = padded_tensor_bytes(p);
+            q = static_cast<const uint8_t*>(workspace) + fwd_bytes;
+            k = static_cast<const uint8_t*>(workspace) + fwd_bytes + tb;
+            s = p;
+            ti = default_strides(p);
+            in = &ti;
+        }
         const Workspace ws = carve(workspace, s, dtype);
         const bool bf16 = dtype == VMB_BF16;
         cudaStream_t st = as_stream(stream);
         const int64_t m = s.m, b = s.b, d = s.d, ud = m * b * d;
-        const float qscale = (float)(1.0 / std::sqrt((double)d));
         if (R) {
             // R of the last R half-step, recomputed from that step's inputs, which the
             // workspace still holds (aR/cR of iteration iters-2, or Q itself when iters == 1).
