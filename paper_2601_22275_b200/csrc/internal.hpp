@@ -171,6 +171,8 @@ struct Tc2Args {
     int64_t oB, oH, oS, oR;
     float* cl_out;               // sum p ln p per row: (u, r, s) at (u*q_len + r)*nseg + s   (nv == 1 only)
     float* lse_out;              // natural-log lse: (u, s, r) at (u*nseg + s)*q_len + r
+    float* ent_out;              // fa3 only: row entropy -sum P ln P, laid out as lse_out (nullptr: off)
+    float* part_ent;             // fa3 split-KV: per-split entropies (n_useg, nsplit, q_len)
     int32_t* status;
     int32_t check_finite;
     // split-KV (attention): fp32 partials (n_useg, nsplit, q_len, 128) + lse (n_useg, nsplit, q_len)

@@ -481,6 +481,18 @@ __global__ void __launch_bounds__(256) fa2_combine_kernel(const Tc2Args a) {
         acc.w = fmaf(w, v.w, acc.w);
     }
     const float inv = 1.f / wsum;
+    if (a.ent_out && lane == 0) {
+        // H = sum_s w_s (H_s - ln w_s), w_s = exp(lse_s - lse) (fa3 split-KV with entropy)
+        const float lse_all = mx + logf(wsum);
+        const float* pe = a.part_ent + (useg * a.nsplit) * rows + r;
+        float h = 0.f;
+        for (int s = 0; s < a.nsplit; ++s) {
+            const float ls = lse[(int64_t)s * rows];
+            const float w = __expf(ls - lse_all);
+            h += w * (pe[(int64_t)s * rows] - (ls - lse_all));
+        }
+        a.ent_out[useg * rows + r] = h;
+    }
     const int64_t ob = u / a.oHn, oh = u % a.oHn;
     __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(a.out) + ob * a.oB + oh * a.oH + (int64_t)seg * a.oS + r * a.oR;
     uint2 v;

@@ -111,7 +111,9 @@ struct Smem {
     static constexpr uint32_t alloc = bytes + 1024;
 };
 
-template <int NB>
+// ENT: also the row entropy H = -sum P ln P = ln2 (lse2 - sum_l 2^(x'_l - m) x'_l / l) in
+// base-2 units x' (flash_entropy.hpp:30-45, 137): one more packed FMA per element pair.
+template <int NB, bool ENT>
 __global__ void __launch_bounds__(kThreads, 1) fa3_kernel(const __grid_constant__ Params p) {
     using SM = Smem<NB>;
     constexpr int S = SM::S;
@@ -275,6 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa3_kernel(const __grid_constant_
         }
 
         float m_run = -INFINITY, l_run = 0.f;
+        float a_run = 0.f;  // ENT: sum_l 2^(x'_l - m_run) x'_l
         const uint64_t scale2x2 = pk2(scale2, scale2);
         for (int j = 0; j < n_kv; ++j) {
             mbar_wait_sleep(&s_full[t], j & 1);
@@ -318,6 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa3_kernel(const __grid_constant_
                     const float m_new = fmaxf(m_run, m_cand);
                     alpha = ex2(m_run - m_new);
                     l_run *= alpha;
+                    if (ENT) a_run *= alpha;
                     m_run = m_new;
                     rescale = true;
                 }
@@ -326,7 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa3_kernel(const __grid_constant_
             // polynomial for the 8th; row sum in packed adds; P -> TMEM as bf16
             const uint64_t negm2 = pk2(-m_run, -m_run);
             const uint64_t* s2 = reinterpret_cast<const uint64_t*>(sr);
-            uint64_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+            uint64_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0, acce = 0;
 #pragma unroll
             for (int cc = 0; cc < kBN / 32; ++cc) {
                 uint32_t pk[16];
@@ -336,6 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa3_kernel(const __grid_constant_
                     uint64_t pp;
                     if ((x % VMB_EMU_PERIOD) == VMB_EMU_PERIOD - 1) pp = ex2_emu2(t2);
                     else pp = pk2(ex2(lo2(t2)), ex2(hi2(t2)));
+                    if (ENT) acce = ffma2(pp, t2, acce);  // sum p (x' - m)
                     switch (x & 3) {
                         case 0: acc0 = fadd2(acc0, pp); break;
                         case 1: acc1 = fadd2(acc1, pp); break;
@@ -347,7 +352,9 @@ __global__ void __launch_bounds__(kThreads, 1) fa3_kernel(const __grid_constant_
                 VMB_TMEM_ST16(tS + cc * 16, pk);
             }
             const uint64_t acc = fadd2(fadd2(acc0, acc1), fadd2(acc2, acc3));
-            l_run += lo2(acc) + hi2(acc);
+            const float tile_l = lo2(acc) + hi2(acc);
+            l_run += tile_l;
+            if (ENT) a_run += (lo2(acce) + hi2(acce)) + m_run * tile_l;  // sum p x' = sum p (x' - m) + m sum p
             if (rescale) {
                 // S_t(j) was issued after PV_t(j-1): O_t is complete here
 #pragma unroll
@@ -370,6 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa3_kernel(const __grid_constant_
         tc_fence_after();
         const float inv_l = 1.f / l_run;
         const float lse2 = m_run + log2f(l_run);  // base-2 log-sum-exp of x' = s * scale2
+        const float ent = ENT ? kLn2 * (lse2 - a_run * inv_l) : 0.f;
         if (a.part_o) {
             // split-KV partial: normalised fp32 O and natural-log lse of this split
             float* prow = a.part_o + (((int64_t)useg * a.nsplit + split) * a.q_len + grow) * 128;
@@ -396,6 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa3_kernel(const __grid_constant_
                 }
             }
             if (valid) a.part_lse[((int64_t)useg * a.nsplit + split) * a.q_len + grow] = kLn2 * lse2;
+            if (ENT && valid) a.part_ent[((int64_t)useg * a.nsplit + split) * a.q_len + grow] = ent;
         } else {
             float qo = 0.f;  // <q_row, O_row> (R-step entropy)
             const int64_t ob = u / a.oHn, oh = u % a.oHn;
@@ -442,6 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa3_kernel(const __grid_constant_
                 if (a.cl_out)
                     a.cl_out[((int64_t)u * a.q_len + grow) * a.nseg + seg] = kLn2 * (scale2 * qo * inv_l - lse2);
                 if (a.lse_out) a.lse_out[((int64_t)u * a.nseg + seg) * a.q_len + grow] = kLn2 * lse2;
+                if (ENT) a.ent_out[((int64_t)u * a.nseg + seg) * a.q_len + grow] = ent;
             }
         }
     }
@@ -457,7 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa3_kernel(const __grid_constant_
 template <int NB>
 void launch(const Params& p, int64_t n_useg, int nsplit, cudaStream_t s) {
     using SM = Smem<NB>;
-    auto kern = fa3_kernel<NB>;
+    auto kern = (NB == 2 && p.a.ent_out) ? fa3_kernel<NB, NB == 2> : fa3_kernel<NB, false>;
     VMB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM::alloc));
     dim3 grid((unsigned)(p.q_pairs * nsplit), (unsigned)n_useg);
     ProfScope ps(NB == 1 ? kKRstep : kKAttn, s);

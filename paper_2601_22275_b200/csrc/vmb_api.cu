@@ -1277,8 +1277,10 @@ vmb_status vmb_flash_entropy_fwd(int64_t units, int64_t nq, int64_t nk, int64_t 
         VMB_REQUIRE_DOMAIN(nk >= 1, "attention over empty keys");
         cudaStream_t st = as_stream(stream);
         const bool bf16 = dtype == VMB_BF16;
-        const bool tc = bf16 && d == 128 && ent == nullptr && tmap_supported() && aligned16(q) && aligned16(k) &&
-                        aligned16(v) && aligned16(o) && nq <= INT32_MAX && nk <= INT32_MAX;
+        // entropy needs the fa3 family (the default); other A/B families run it on CUDA cores
+        const bool tc = bf16 && d == 128 && (ent == nullptr || attn_impl(false) == 3) && tmap_supported() &&
+                        aligned16(q) && aligned16(k) && aligned16(v) && aligned16(o) && nq <= INT32_MAX &&
+                        nk <= INT32_MAX;
         if (tc) {
             Tc2Args f2{};
             const uint32_t bn = attn_kv_box(false);
@@ -1301,15 +1303,17 @@ vmb_status vmb_flash_entropy_fwd(int64_t units, int64_t nq, int64_t nk, int64_t 
             f2.out = o;
             f2.oB = nq * d; f2.oH = 0; f2.oS = 0; f2.oR = d;
             f2.lse_out = lse;
+            f2.ent_out = ent;
             const int nsplit = attn_plan_splits(nq, nk, units);
             float* part = nullptr;
             int32_t* dummy = nullptr;
             VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dummy), sizeof(int32_t), st));
             if (nsplit > 1) {
                 VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part),
-                                               (size_t)units * nsplit * nq * 129 * sizeof(float), st));
+                                               (size_t)units * nsplit * nq * 130 * sizeof(float), st));
                 f2.part_o = part;
                 f2.part_lse = part + (size_t)units * nsplit * nq * 128;
+                f2.part_ent = part + (size_t)units * nsplit * nq * 129;
                 f2.max_split = kTc2MaxSplit;
             } else {
                 f2.max_split = 1;

@@ -184,3 +184,23 @@ def test_dense_forward_parity(vm, orc, cuda):
     got = vm.dense_forward(*(torch.from_numpy(x).to(cuda, torch.bfloat16) for x in (q, k, v)))
     ref = orc.dense_forward(q[0], k[0], v[0])
     assert relfro(got[0].float().cpu().numpy(), ref) <= BF16_TOL
+
+
+@pytest.mark.parametrize("U,nq,nk", [(2, 300, 1000), (1, 100, 20000), (3, 257, 4100)])
+def test_flash_entropy_bf16_tcgen05(vm, orc, cuda, U, nq, nk):
+    """bf16 / d = 128 flash_entropy_fwd with entropy on the tcgen05 kernel (fa3): the row
+    entropy accumulates sum p x' beside the row sum; split-KV partial entropies combine as
+    H = sum_s w_s (H_s - ln w_s).  (1, 100, 20000) takes the split path."""
+    d = 128
+    q = bf16_round(randn((U, nq, d), 41, dtype=np.float32) / np.sqrt(d))
+    k = bf16_round(randn((U, nk, d), 42, dtype=np.float32))
+    v = bf16_round(randn((U, nk, d), 43, dtype=np.float32))
+    launches = vm.kernel_launch_count()
+    o, lse, ent = vm.flash_entropy_fwd(*(torch.from_numpy(x).to(cuda, torch.bfloat16) for x in (q, k, v)))
+    torch.cuda.synchronize()
+    assert vm.kernel_launch_count() > launches
+    for u in range(U):
+        ro, rl, re = orc.flash_entropy_fwd(q[u], k[u], v[u])
+        assert relfro(o[u].float().cpu().numpy(), ro) <= BF16_TOL
+        assert np.abs(lse[u].cpu().numpy() - rl).max() <= 1e-3
+        assert np.abs(ent[u].cpu().numpy() - re).max() <= 1e-3
