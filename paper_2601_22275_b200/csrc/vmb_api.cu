@@ -1227,9 +1227,40 @@ vmb_status vmb_lstep(int64_t units, int64_t m, int64_t b, int64_t d, vmb_dtype d
         cudaStream_t st = as_stream(stream);
         const bool bf16 = dtype == VMB_BF16;
         const int64_t ud = m * b * d;
-        const bool tc = bf16 && d == 128 && m <= 128 && L == nullptr && tmap_supported() && aligned16(Qb) &&
+        const bool tc = bf16 && d == 128 && L == nullptr && tmap_supported() && aligned16(Qb) &&
                         aligned16(aL) && aligned16(aR);
         (void)ceil16;
+        if (tc && m > 128) {
+            // more than 128 row blocks: the multi-pass L-step (lstep_big.cu) with lse2 scratch
+            auto qmap = [&](uint32_t rows) {
+                const uint64_t dims[5] = {(uint64_t)d, (uint64_t)b, (uint64_t)m, 1, (uint64_t)std::max<int64_t>(units, 1)};
+                const uint64_t strides[4] = {(uint64_t)(m * d * 2), (uint64_t)(d * 2), (uint64_t)(ud * 2), (uint64_t)(ud * 2)};
+                const uint32_t box[5] = {64, 1, rows, 1, 1};
+                return make_tmap_bf16_5d(Qb, dims, strides, box);
+            };
+            TcLstepBigArgs lb{};
+            lb.tmQ128 = qmap(128);
+            lb.tmQ64 = qmap(64);
+            lb.tmAL128 = internal_map(aL, units, b, m, d, true, 128, 1);
+            lb.tmAL64 = internal_map(aL, units, b, m, d, true, 64, 1);
+            lb.tmY64 = lb.tmAL64;  // unused (ITER)
+            float* lse2 = nullptr;
+            if (units > 0)
+                VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&lse2), sizeof(float) * units * m * b, st));
+            lb.cL = cL;
+            lb.lse2 = lse2;
+            lb.cR = cR;
+            lb.aR = static_cast<__nv_bfloat16*>(aR);
+            lb.qscale = 1.f;
+            lb.out_scale = 1.f;
+            lb.m = (int32_t)m;
+            lb.b = (int32_t)b;
+            lb.H = 1;
+            lb.oHn = 1;
+            tc_lstep_big_launch(lb, units, false, st);
+            if (lse2) VMB_CHECK_CUDA(cudaFreeAsync(lse2, st));
+            return;
+        }
         if (tc) {
             TcLstepArgs ls{};
             const uint32_t lrows = (uint32_t)lstep_rows(m);

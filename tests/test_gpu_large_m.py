@@ -43,3 +43,19 @@ def test_b1_factorization_equals_dense_at_8k(vm, cuda):
     dense = vm.dense_forward(q, k, v)
     torch.cuda.synchronize()
     assert relfro(out.float().cpu().numpy(), dense.float().cpu().numpy()) <= 2e-2
+
+
+@pytest.mark.parametrize("m,b", [(200, 3), (256, 2)])
+def test_large_m_lstep_half_step_parity(vm, orc, cuda, m, b):
+    # vmb_lstep with m > 128 (bf16, d = 128) runs the multi-pass L-step; the oracle l_update
+    rng = np.random.default_rng(3)
+    Qb = bf16_round(rng.standard_normal((2, b, m, 128)).astype(np.float32) / np.sqrt(128))
+    aL = bf16_round(rng.standard_normal((2, b, m, 128)).astype(np.float32))
+    cL = (-np.log(m) + 0.3 * rng.standard_normal((2, b, m))).astype(np.float32)
+    aR, cR, _ = vm.l_update(torch.from_numpy(Qb).to(cuda, torch.bfloat16), torch.from_numpy(aL).to(cuda, torch.bfloat16),
+                            torch.from_numpy(cL).to(cuda))
+    torch.cuda.synchronize()
+    for u in range(2):
+        raR, rcR, _ = orc.lstep(Qb[u], aL[u], cL[u], want_L=False)
+        assert relfro(aR[u].float().cpu().numpy(), raR) <= 2e-2
+        assert relfro(cR[u].cpu().numpy(), rcR) <= 2e-2
