@@ -53,18 +53,8 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
     asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
     return d;
 }
-// 2^x on the FMA/ALU pipes (see fa_tc.cu): rel. err 1.1e-4, far below the bf16 P rounding.
-__device__ __forceinline__ float ex2_emu(float x) {
-    x = fmaxf(x, -126.f);
-    const float kMagic = 12582912.f;
-    const float t = x + kMagic;
-    const float f = x - (t - kMagic);
-    const float p = fmaf(fmaf(fmaf(0.05592203512787819f, f, 0.24264007806777954f), f, 0.6931210160255432f), f,
-                         0.9999244809150696f);
-    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
 
-// packed variant of ex2_emu for an element pair (FADD2/FFMA2 + integer exponent add)
+// 2^x for an element pair on the FMA/ALU pipes (FADD2/FFMA2 + integer exponent add; see fa3_tc.cu)
 __device__ __forceinline__ uint64_t ex2_emu2(uint64_t x2);
 
 struct Params {
