@@ -11,10 +11,15 @@ Reference -> here
   vmonarch_attention<T> (video.hpp:84-150)              vmonarch_attention
   r_update / l_update (monarch.hpp:53-147)              r_update / l_update
   flash_entropy_fwd (flash_entropy.hpp:85-139)          flash_entropy_fwd
+  flash_entropy_bwd (flash_entropy.hpp:141-221)         flash_entropy_bwd
   dense_forward (oracle.hpp:36-72)                      dense_forward
   factorize / flops_estimate (video.cpp:13-59)          factorize / flops_estimate
   make_perm (perm.hpp:19-30)                            make_perm
   std::invalid_argument / domain_error / logic_error    DimensionError / DomainError / StateError
+Beyond the reference API: vmonarch_attention_host (host buffers, pipelined H2D / forward /
+D2H), vmonarch_attention_slab + seq_assemble (sequence sharding, one process per GPU),
+vmonarch_attention_multi (one process, several GPUs), torch_op (DiT integration), dist
+(partitions and NCCL collectives), matn (MATN files).
 """
 from __future__ import annotations
 
@@ -31,7 +36,7 @@ __all__ = [
     "vmonarch_attention", "r_update", "l_update", "flash_entropy_fwd", "dense_forward",
     "factorize", "flops_estimate", "make_perm", "preset_grid", "export_factors", "lib",
     "kernel_launch_count", "LIB_PATH", "vmonarch_attention_slab", "seq_assemble", "vmonarch_attention_host",
-    "flash_entropy_bwd",
+    "flash_entropy_bwd", "vmonarch_attention_multi", "shard_range", "SHARD_MODES", "CudaError",
 ]
 
 LIB_PATH = os.environ.get("VMB_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libvmb.so")
