@@ -26,8 +26,8 @@ KEYS = [("fa_tc_kernel<2, 2", "rstep_y"), ("fa_tc_kernel<1, 1", "rstep"), ("fa2_
         ("fa2_kernel<2>", "attn_recompute"), ("fa3_kernel<2", "attn_recompute"), ("fa3_kernel<1", "rstep"),
         ("fa4_kernel<1, 1>", "rstep"), ("fa4_kernel<2, 2>", "rstep_y"), ("fa4_kernel<2, 1>", "attn_recompute"),
         ("fa6_kernel<2", "attn_recompute"), ("fa6_kernel<1", "rstep"),
-        ("lstep_tc_kernel<0", "lstep"), ("lstep_tc_kernel<1", "lstep_apply"), ("lstep_big_kernel<1", "lstep"),
-        ("lstep_big_kernel<2", "lstep_apply"), ("lstep_big_kernel<0", "lstep_rowstat"), ("fa2_combine", "combine"),
+        ("lstep_tc_kernel<0", "lstep"), ("lstep_tc_kernel<1", "lstep_apply"), ("lstep_big_kernel<1", "lstep_big_iter"),
+        ("lstep_big_kernel<2", "lstep_big_final"), ("lstep_big_kernel<0", "lstep_big_rowstat"), ("fa2_combine", "combine"),
         ("seq_assemble", "seq_assemble"), ("peer_gather", "peer_gather"), ("pad_rows", "pad_rows"),
         ("bwd_dq_kernel", "bwd_dq"), ("bwd_dkv_kernel", "bwd_dkv"), ("bwd_rowstat", "bwd_rowstat")]
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
