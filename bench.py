@@ -38,6 +38,8 @@ CONFIGS = {
     "c3": (21, 30, 52, 40, 128, "C3: Wan-2.1-14B 21x30x52 latent (N=32760), H=40, d=128, bf16, t=2"),
     "c2": (21, 30, 52, 12, 128, "C2: Wan-2.1-1.3B 21x30x52 latent (N=32760), H=12, d=128, bf16, t=2"),
     "c5": (81, 112, 104, 40, 128, "C5: long-video stress 81x112x104 latent (N=943488), H=40, d=128, bf16, t=2"),
+    # the reference's CPU-runnable case (BASELINE configs[0] shape) for quick contract checks
+    "c1": (4, 8, 8, 2, 64, "C1: oracle-check shape 4x8x8 (N=256), H=2, d=64, bf16, t=2"),
 }
 KERNEL_NAMES = ["rstep", "rstep_y", "attn_recompute", "lstep", "lstep_apply", "simt", "combine"]
 
