@@ -131,9 +131,11 @@ __global__ void __launch_bounds__(kThreads, 2) fa2_kernel(const __grid_constant_
 
     const Tc2Args& a = p.a;
     const int warp = warp_id();
-    const int qtile = blockIdx.x % p.q_tiles;
-    const int split = blockIdx.x / p.q_tiles;
-    const int useg = blockIdx.y;  // u * nseg + seg
+    // 1-D grid, (useg, split, qtile) with qtile fastest: no 65535 limit on units x segments
+    const int per = p.q_tiles * p.a.nsplit;
+    const int useg = (int)(blockIdx.x / (unsigned)per);  // u * nseg + seg
+    const int qtile = (int)(blockIdx.x % (unsigned)per) % p.q_tiles;
+    const int split = (int)(blockIdx.x % (unsigned)per) / p.q_tiles;
     const int u = useg / a.nseg, seg = useg % a.nseg;
     const int kv_tile0 = split * p.n_kv_tiles;
     const int n_kv = min(p.n_kv_tiles, p.total_tiles - kv_tile0);
@@ -497,7 +499,8 @@ void launch(const Params& p, int64_t n_useg, int nsplit, cudaStream_t s) {
     using SM = Smem<NB>;
     auto kern = fa2_kernel<NB>;
     VMB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM::alloc));
-    dim3 grid((unsigned)(p.q_tiles * nsplit), (unsigned)n_useg);
+    VMB_REQUIRE_DIM((int64_t)p.q_tiles * nsplit * n_useg <= (int64_t)INT32_MAX, "attention grid too large");
+    const dim3 grid((unsigned)((int64_t)p.q_tiles * nsplit * n_useg));
     ProfScope ps(NB == 1 ? kKRstep : kKAttn, s);
     kern<<<grid, kThreads, SM::alloc, s>>>(p);
     count_launch();

@@ -413,8 +413,8 @@ bool tc_eligible(const Shape& s, vmb_dtype dt, const vmb_strides& in, const vmb_
                  const void* q, const void* k, const void* v, const void* o) {
     if (dt != VMB_BF16 || s.d != 128 || !tmap_supported()) return false;
     if (s.N > (int64_t)INT32_MAX || s.b > 65535 * 16) return false;
-    // the R-step grids put (unit, frame block) on grid.y
-    if (s.U * s.m > 65535) return false;
+    // the default R-step grid is 1-D; the A/B families put (unit, frame block) on grid.y
+    if (attn_impl(true) != 2 && s.U * s.m > 65535) return false;
     const int64_t strides[6] = {in.batch, in.head, in.token, out.batch, out.head, out.token};
     for (int64_t x : strides)
         if (x % 8 != 0) return false;
@@ -714,7 +714,8 @@ int64_t ceil16(int64_t x) { return (x + 15) & ~int64_t(15); }
 // with Q, K, V zero-padded to 128 columns in the workspace: zero columns add nothing to any
 // score or product, so every half-step is exact, and the padded output columns are dropped.
 bool padded_path(const Shape& s, vmb_dtype dt) {
-    return dt == VMB_BF16 && s.d < 128 && tmap_supported() && s.U * s.m <= 65535 && s.N <= (int64_t)INT32_MAX;
+    return dt == VMB_BF16 && s.d < 128 && tmap_supported() && (attn_impl(true) == 2 || s.U * s.m <= 65535) &&
+           s.N <= (int64_t)INT32_MAX;
 }
 Shape padded_shape(const Shape& s) {
     Shape p = s;

@@ -59,3 +59,15 @@ def test_large_m_lstep_half_step_parity(vm, orc, cuda, m, b):
         raR, rcR, _ = orc.lstep(Qb[u], aL[u], cL[u], want_L=False)
         assert relfro(aR[u].float().cpu().numpy(), raR) <= 2e-2
         assert relfro(cR[u].cpu().numpy(), rcR) <= 2e-2
+
+
+def test_b1_factorization_many_row_blocks_on_tensor_cores(vm, cuda):
+    # (m, b) = (N, 1) with units x m > 65535: the 1-D R-step grid and the multi-pass L-step;
+    # b = 1 reduces VMonarch to dense attention (test_monarch_core.cpp:285-309)
+    grid = vm.TokenGrid(8, 32, 64, 128, 5, 1)  # N = 16384, 5 units -> 81920 (unit, row block) pairs
+    g = torch.Generator(device=cuda).manual_seed(8)
+    q, k, v = (torch.randn((5, grid.tokens(), 128), generator=g, device=cuda).to(torch.bfloat16) for _ in range(3))
+    out = vm.vmonarch_attention(q, k, v, grid, vm.VMonarchConfig(override_m_b=(grid.tokens(), 1)))
+    dense = vm.dense_forward(q, k, v)
+    torch.cuda.synchronize()
+    assert relfro(out.float().cpu().numpy(), dense.float().cpu().numpy()) <= 2e-2
