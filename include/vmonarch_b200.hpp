@@ -32,8 +32,8 @@
 
 #include <cmath>
 #include <cstdint>
-#include <utility>
 #include <cstring>
+#include <utility>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -220,13 +220,38 @@ ResultT flash_entropy_bwd(const MatT& q, const MatT& k, const MatT& v, const Mat
 }
 
 // ---------------------------------------------------------------- the operator (video.hpp:84-150)
+// Compute precision of the façade.  fp32 (default) is the parity mode: <= 1e-4 of the
+// reference, on CUDA cores.  bf16 rounds the float inputs to bf16 on the host and runs the
+// tcgen05 path (the performance path, <= 2e-2 of the reference; 100-700x faster than fp32 at
+// the Wan shapes), returning float outputs.  An extra trailing argument, so calls written
+// for the reference signature are unchanged.
+enum class Precision { fp32, bf16 };
+
+namespace detail {
+inline uint16_t f32_to_bf16(float f) {
+    uint32_t x;
+    std::memcpy(&x, &f, 4);
+    if ((x & 0x7F800000u) == 0x7F800000u) return (uint16_t)((x >> 16) | ((x & 0xFFFFu) ? 0x40u : 0u));  // inf / NaN
+    return (uint16_t)((x + 0x7FFFu + ((x >> 16) & 1u)) >> 16);  // round to nearest even
+}
+inline float bf16_to_f32(uint16_t h) {
+    const uint32_t x = (uint32_t)h << 16;
+    float f;
+    std::memcpy(&f, &x, 4);
+    return f;
+}
+}  // namespace detail
+
 template <class MatT, class GridT, class CfgT, class FactorsVec = std::vector<int>>
 std::vector<MatT> vmonarch_attention(std::span<const MatT> qs, std::span<const MatT> ks, std::span<const MatT> vs,
                                      const GridT& grid, const CfgT& cfg, int threads = 1,
-                                     FactorsVec* factors_out = nullptr) {
+                                     FactorsVec* factors_out = nullptr, Precision prec = Precision::fp32) {
     (void)threads;
     using T = typename std::remove_cv_t<std::remove_reference_t<decltype(qs[0].data[0])>>;
-    static_assert(std::is_same_v<T, float>, "the drop-in façade runs the fp32 parity mode (T = float)");
+    static_assert(std::is_same_v<T, float>, "the drop-in façade takes the reference's T = float matrices");
+    const bool bf16 = prec == Precision::bf16;
+    const vmb_dtype dt = bf16 ? VMB_BF16 : VMB_F32;
+    const size_t es = bf16 ? 2 : 4;
     const int64_t units = (int64_t)grid.heads * (int64_t)grid.batch;
     check_dim((int64_t)qs.size() == units && (int64_t)ks.size() == units && (int64_t)vs.size() == units,
               "expected one Q/K/V matrix per batch*head unit");
@@ -240,36 +265,44 @@ std::vector<MatT> vmonarch_attention(std::span<const MatT> qs, std::span<const M
     int64_t m = 0, b = 0;
     check(vmb_factorize(&g, &c, &m, &b));
 
-    const size_t unit_bytes = (size_t)n * d * sizeof(float);
+    const size_t unit_elems = (size_t)n * d, unit_bytes = unit_elems * es;
     DeviceBuffer dq(unit_bytes * units), dk(unit_bytes * units), dv(unit_bytes * units), dout(unit_bytes * units);
+    std::vector<uint16_t> stage(bf16 ? unit_elems : 0);
+    auto upload = [&](const MatT& m, void* dst, const char* what) {
+        const void* src = m.data.data();
+        if (bf16) {
+            for (size_t x = 0; x < unit_elems; ++x) stage[x] = detail::f32_to_bf16(m.data[x]);
+            src = stage.data();
+        }
+        check_cuda(cudaMemcpy(dst, src, unit_bytes, cudaMemcpyHostToDevice), what);
+    };
     for (int64_t u = 0; u < units; ++u) {
-        check_cuda(cudaMemcpy((char*)dq.get() + u * unit_bytes, qs[u].data.data(), unit_bytes, cudaMemcpyHostToDevice),
-                   "H2D q");
-        check_cuda(cudaMemcpy((char*)dk.get() + u * unit_bytes, ks[u].data.data(), unit_bytes, cudaMemcpyHostToDevice),
-                   "H2D k");
-        check_cuda(cudaMemcpy((char*)dv.get() + u * unit_bytes, vs[u].data.data(), unit_bytes, cudaMemcpyHostToDevice),
-                   "H2D v");
+        upload(qs[u], (char*)dq.get() + u * unit_bytes, "H2D q");
+        upload(ks[u], (char*)dk.get() + u * unit_bytes, "H2D k");
+        upload(vs[u], (char*)dv.get() + u * unit_bytes, "H2D v");
     }
-    const size_t ws_bytes = vmb_workspace_size(&g, &c, VMB_F32);
+    const size_t ws_bytes = vmb_workspace_size(&g, &c, dt);
     if (ws_bytes == 0) raise_status(VMB_ERR_DIM);
     DeviceBuffer ws(ws_bytes);
-    check(vmb_vmonarch_fwd(&g, &c, VMB_F32, dq.get(), dk.get(), dv.get(), dout.get(), nullptr, nullptr, ws.get(),
-                           ws_bytes, nullptr));
+    check(vmb_vmonarch_fwd(&g, &c, dt, dq.get(), dk.get(), dv.get(), dout.get(), nullptr, nullptr, ws.get(), ws_bytes,
+                           nullptr));
     check(vmb_workspace_status(ws.get(), nullptr));  // device-raised domain errors (monarch.hpp:44, 78)
 
     std::vector<MatT> out;
     out.reserve((size_t)units);
     for (int64_t u = 0; u < units; ++u) {
         out.emplace_back(n, d);
-        check_cuda(cudaMemcpy(out.back().data.data(), (char*)dout.get() + u * unit_bytes, unit_bytes,
-                              cudaMemcpyDeviceToHost),
+        void* dst = bf16 ? (void*)stage.data() : (void*)out.back().data.data();
+        check_cuda(cudaMemcpy(dst, (char*)dout.get() + u * unit_bytes, unit_bytes, cudaMemcpyDeviceToHost),
                    "D2H out");
+        if (bf16)
+            for (size_t x = 0; x < unit_elems; ++x) out.back().data[x] = detail::bf16_to_f32(stage[x]);
     }
     if constexpr (!std::is_same_v<FactorsVec, std::vector<int>>) {
         if (factors_out) {
             // MonarchFactors (monarch.hpp:12-19): L (b, m, m), R (m, b, b) per unit
             DeviceBuffer dL((size_t)units * b * m * m * sizeof(float)), dR((size_t)units * m * b * b * sizeof(float));
-            check(vmb_export_factors(&g, &c, VMB_F32, dq.get(), dk.get(), nullptr, ws.get(), (float*)dL.get(),
+            check(vmb_export_factors(&g, &c, dt, dq.get(), dk.get(), nullptr, ws.get(), (float*)dL.get(),
                                      (float*)dR.get(), nullptr));
             check_cuda(cudaDeviceSynchronize(), "factor export");
             factors_out->resize((size_t)units);

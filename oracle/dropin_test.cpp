@@ -106,6 +106,28 @@ int main() {
     parity_case("batch 2 x heads 2, d=16", vmonarch::TokenGrid{5, 4, 4, 16, 2, 2}, vmonarch::VMonarchConfig{}, 3.0,
                 false);
 
+    // bf16 performance mode of the façade (Precision::bf16): float in / float out on the tcgen05 path
+    {
+        for (auto g : {vmonarch::TokenGrid{4, 8, 8, 64, 2, 1}, vmonarch::TokenGrid{4, 8, 16, 128, 2, 1},
+                       vmonarch::TokenGrid{21, 6, 7, 128, 1, 1}}) {
+            const long n = g.tokens();
+            auto qs = randn_units((int)g.units(), n, g.head_dim, 200, 1.0);
+            auto ks = randn_units((int)g.units(), n, g.head_dim, 201, 1.0);
+            auto vs = randn_units((int)g.units(), n, g.head_dim, 202, 1.0);
+            std::span<const Mat<float>> sq(qs), sk(ks), sv(vs);
+            vmonarch::VMonarchConfig cf;
+            auto ref = vmonarch::vmonarch_attention<float>(sq, sk, sv, g, cf, 4);
+            std::vector<vmonarch::MonarchFactors<float>>* none = nullptr;
+            auto got = vmonarch_b200::vmonarch_attention(sq, sk, sv, g, cf, 4, none, vmonarch_b200::Precision::bf16);
+            double worst = 0;
+            for (size_t u = 0; u < ref.size(); ++u) worst = std::max(worst, relfro(got[u].data, ref[u].data));
+            char buf[200];
+            std::snprintf(buf, sizeof buf, "bf16 mode %ldx%ldx%ld d=%ld: output rel-Fro %.2e (<= 2e-2)", (long)g.t_frames,
+                          (long)g.h, (long)g.w, (long)g.head_dim, worst);
+            expect(worst <= 2e-2, buf);
+        }
+    }
+
     // companions: monarch_attention, flash_entropy_fwd / _bwd, dense_forward, flops_estimate
     {
         auto q = randn_units(1, 256, 32, 40, 1.0)[0], k = randn_units(1, 256, 32, 41, 1.0)[0],
