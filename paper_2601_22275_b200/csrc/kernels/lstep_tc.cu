@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
 #pragma unroll
             for (int e = 0; e < 8; ++e) col[e] += lj(j + e);
         }
-        for (; j < m; ++j) col[j & 7] += lj(j);
+        for (; j < m; ++j) col[0] += lj(j);  // (static index: col[] stays in registers)
         a.cR[((int64_t)u * m + t) * a.b + i] = ((col[0] + col[1]) + (col[2] + col[3])) + ((col[4] + col[5]) + (col[6] + col[7]));
     }
 
