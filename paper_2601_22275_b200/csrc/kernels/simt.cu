@@ -113,6 +113,54 @@ __global__ void __launch_bounds__(BLOCK) simt_rstep_kernel(SimtRstepArgs a) {
     }
     const float qs = a.qscale;
 
+    if (!a.R) {
+        // One pass with running statistics (no R export requested): max m, sum l and
+        // A = sum e s in double (monarch.hpp:87-98 accumulate in double), acc = sum e V in fp32,
+        // rescaled whenever the row max grows.  Then aL = acc / l and
+        // cL = sum p ln p = A / l - m - ln l.  Same quantities as the three passes below, a
+        // third of the dot products.
+        float m_run = -INFINITY;
+        double l_run = 0.0, a_run = 0.0;
+        float acc[DPT];
+#pragma unroll
+        for (int x = 0; x < DPT; ++x) acc[x] = 0.f;
+        float* smv = sm + KTILE * d;
+        for (int64_t l0 = 0; l0 < a.b; l0 += KTILE) {
+            __syncthreads();
+            stage_rows<T>(sm, a.K, u, k, l0, a.b, d);
+            stage_rows<T>(smv, a.V, u, k, l0, a.b, d);
+            __syncthreads();
+            const int nl = (int)((a.b - l0) < KTILE ? (a.b - l0) : KTILE);
+            for (int r = 0; r < nl; ++r) {
+                const float sv = (dot_smem<G>(q, sm + r * d, d0, d) * qs) * inv_c;
+                if (sv > m_run) {
+                    const float sc = expf(m_run - sv);  // 0 on the first key
+                    l_run *= sc;
+                    a_run *= sc;
+#pragma unroll
+                    for (int x = 0; x < DPT; ++x) acc[x] *= sc;
+                    m_run = sv;
+                }
+                const float e = expf(sv - m_run);
+                l_run += (double)e;
+                a_run += (double)e * (double)sv;
+                const float* vr = smv + r * d;
+#pragma unroll
+                for (int x = 0; x < DPT; ++x)
+                    if (d0 + x < d) acc[x] = fmaf(e, vr[d0 + x], acc[x]);
+            }
+        }
+        if (!valid) return;
+        const float inv_l = (float)(1.0 / l_run);
+        T* out = static_cast<T*>(const_cast<void*>(a.Out.base)) + row_off(a.Out, u, k, i);
+#pragma unroll
+        for (int x = 0; x < DPT; ++x)
+            if (d0 + x < d) st1(out + d0 + x, acc[x] * inv_l);
+        if (a.cL && g == 0) a.cL[(u * a.b + i) * a.m + k] = (float)(a_run / l_run - (double)m_run - log(l_run));
+        return;
+    }
+
+    // R export: the reference's three passes (the exported R rows need the final max and sum)
     // pass 1: row max of logits * inv_c   (monarch.hpp:81-86)
     float mx = -INFINITY;
     for (int64_t l0 = 0; l0 < a.b; l0 += KTILE) {
