@@ -117,6 +117,11 @@ struct SimtFlashArgs {
     float* lse;        // (U, nq) or nullptr
     float* ent;        // (U, nq) or nullptr
     int64_t U, nq, nk, d;
+    // split-KV (set by simt_flash): key range split `blockIdx.z` of `nsplit`; partial rows
+    // (unnormalised acc, fp32) and statistics (max, sum, entropy accumulator; double)
+    int32_t nsplit = 1;
+    float* part_acc = nullptr;     // (nsplit, U, nq, d)
+    double* part_stat = nullptr;   // (nsplit, U, nq, 3)
 };
 void simt_rstep(const SimtRstepArgs& a, bool bf16, cudaStream_t s);
 void simt_lstep(const SimtLstepArgs& a, bool bf16, cudaStream_t s);

@@ -347,6 +347,9 @@ __global__ void __launch_bounds__(BLOCK) simt_flash_kernel(SimtFlashArgs a) {
     const int64_t r = (int64_t)blockIdx.x * RPB + rloc;
     const bool valid = r < a.nq;
     const int d = (int)a.d, d0 = g * DPT;
+    // key range of this split
+    const int64_t chunk = (a.nk + a.nsplit - 1) / a.nsplit;
+    const int64_t kb = (int64_t)blockIdx.z * chunk, ke = kb + chunk < a.nk ? kb + chunk : a.nk;
     float q[DPT], acc[DPT];
     if (valid) {
         load_slice(static_cast<const T*>(a.Q.base) + row_off(a.Q, u, 0, r), d0, d, a.qscale, q);
@@ -357,12 +360,12 @@ __global__ void __launch_bounds__(BLOCK) simt_flash_kernel(SimtFlashArgs a) {
 #pragma unroll
     for (int x = 0; x < DPT; ++x) acc[x] = 0.f;
     double run_max = -INFINITY, norm = 0.0, ent = 0.0;
-    for (int64_t l0 = 0; l0 < a.nk; l0 += KTILE) {
+    for (int64_t l0 = kb; l0 < ke; l0 += KTILE) {
         __syncthreads();
-        stage_rows<T>(smk, a.K, u, 0, l0, a.nk, d);
-        stage_rows<T>(smv, a.V, u, 0, l0, a.nk, d);
+        stage_rows<T>(smk, a.K, u, 0, l0, ke, d);
+        stage_rows<T>(smv, a.V, u, 0, l0, ke, d);
         __syncthreads();
-        const int nl = (int)((a.nk - l0) < KTILE ? (a.nk - l0) : KTILE);
+        const int nl = (int)((ke - l0) < KTILE ? (ke - l0) : KTILE);
         float s[KTILE];
         double tmax = -INFINITY;
 #pragma unroll
@@ -399,6 +402,20 @@ __global__ void __launch_bounds__(BLOCK) simt_flash_kernel(SimtFlashArgs a) {
         run_max = m_new;
     }
     if (!valid) return;
+    if (a.nsplit > 1) {
+        // split-KV partial: unnormalised acc and (max, sum, entropy accumulator)
+        const int64_t pr = ((int64_t)blockIdx.z * a.U + u) * a.nq + r;
+        float* pa = a.part_acc + pr * d;
+#pragma unroll
+        for (int x = 0; x < DPT; ++x)
+            if (d0 + x < d) pa[d0 + x] = acc[x];
+        if (g == 0) {
+            a.part_stat[pr * 3 + 0] = run_max;
+            a.part_stat[pr * 3 + 1] = norm;
+            a.part_stat[pr * 3 + 2] = ent;
+        }
+        return;
+    }
     const float inv = (float)(1.0 / norm);
     T* out = static_cast<T*>(const_cast<void*>(a.O.base)) + row_off(a.O, u, 0, r);
 #pragma unroll
@@ -406,6 +423,46 @@ __global__ void __launch_bounds__(BLOCK) simt_flash_kernel(SimtFlashArgs a) {
         if (d0 + x < d) st1(out + d0 + x, acc[x] * inv);
     if (g == 0) {
         if (a.lse) a.lse[u * a.nq + r] = (float)(run_max + log(norm));
+        if (a.ent) a.ent[u * a.nq + r] = (float)(log(norm) - ent / norm);
+    }
+}
+
+// Merge of the split-KV partials (same statistics as the single pass, flash_entropy.hpp:30-45):
+// m = max m_s, l = sum l_s e^(m_s - m), E = sum e^(m_s - m) (E_s + (m_s - m) l_s), O = acc / l.
+template <typename T, int G>
+__global__ void __launch_bounds__(BLOCK) simt_flash_combine_kernel(SimtFlashArgs a) {
+    constexpr int RPB = BLOCK / G;
+    const int g = threadIdx.x % G, rloc = threadIdx.x / G;
+    const int64_t u = blockIdx.y;
+    const int64_t r = (int64_t)blockIdx.x * RPB + rloc;
+    if (r >= a.nq) return;
+    const int d = (int)a.d, d0 = g * DPT;
+    double m = -INFINITY;
+    for (int s = 0; s < a.nsplit; ++s) m = fmax(m, a.part_stat[(((int64_t)s * a.U + u) * a.nq + r) * 3]);
+    double norm = 0.0, ent = 0.0;
+    float acc[DPT];
+#pragma unroll
+    for (int x = 0; x < DPT; ++x) acc[x] = 0.f;
+    for (int s = 0; s < a.nsplit; ++s) {
+        const int64_t pr = ((int64_t)s * a.U + u) * a.nq + r;
+        const double ms = a.part_stat[pr * 3 + 0], ls = a.part_stat[pr * 3 + 1], es = a.part_stat[pr * 3 + 2];
+        if (isinf(ms)) continue;  // empty split
+        const double w = exp(ms - m);
+        norm += w * ls;
+        ent += w * (es + (ms - m) * ls);
+        const float wf = (float)w;
+        const float* pa = a.part_acc + pr * d;
+#pragma unroll
+        for (int x = 0; x < DPT; ++x)
+            if (d0 + x < d) acc[x] = fmaf(wf, pa[d0 + x], acc[x]);
+    }
+    const float inv = (float)(1.0 / norm);
+    T* out = static_cast<T*>(const_cast<void*>(a.O.base)) + row_off(a.O, u, 0, r);
+#pragma unroll
+    for (int x = 0; x < DPT; ++x)
+        if (d0 + x < d) st1(out + d0 + x, acc[x] * inv);
+    if (g == 0) {
+        if (a.lse) a.lse[u * a.nq + r] = (float)(m + log(norm));
         if (a.ent) a.ent[u * a.nq + r] = (float)(log(norm) - ent / norm);
     }
 }
@@ -467,15 +524,34 @@ void lstep_launch(const SimtLstepArgs& a, cudaStream_t s) {
     check_launch("simt_lstep");
 }
 template <typename T, int G>
-void flash_launch(const SimtFlashArgs& a, cudaStream_t s) {
+void flash_launch(const SimtFlashArgs& a0, cudaStream_t s) {
     constexpr int RPB = BLOCK / G;
-    dim3 grid((unsigned)((a.nq + RPB - 1) / RPB), (unsigned)a.U);
+    SimtFlashArgs a = a0;
+    const int64_t row_blocks = (a.nq + RPB - 1) / RPB;
+    // split the keys when the row blocks of one unit fill less than two waves; the split count
+    // depends on the per-unit shape only (bitwise-identical results for any unit count)
+    a.nsplit = (int32_t)std::max<int64_t>(1, std::min<int64_t>({(2 * 148 + row_blocks - 1) / row_blocks, 32,
+                                                                 a.nk / (8 * KTILE)}));
+    if (a.nsplit > 1) {
+        VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.part_acc),
+                                       sizeof(float) * a.nsplit * a.U * a.nq * a.d, s));
+        VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.part_stat),
+                                       sizeof(double) * 3 * a.nsplit * a.U * a.nq, s));
+    }
+    const dim3 grid((unsigned)row_blocks, (unsigned)a.U, (unsigned)a.nsplit);
     const size_t smem = 2 * KTILE * a.d * sizeof(float);
     set_smem(simt_flash_kernel<T, G>, smem);
     ProfScope ps(kKSimt, s);
     simt_flash_kernel<T, G><<<grid, BLOCK, smem, s>>>(a);
     count_launch();
     check_launch("simt_flash");
+    if (a.nsplit > 1) {
+        simt_flash_combine_kernel<T, G><<<dim3((unsigned)row_blocks, (unsigned)a.U), BLOCK, 0, s>>>(a);
+        count_launch();
+        check_launch("simt_flash_combine");
+        VMB_CHECK_CUDA(cudaFreeAsync(a.part_acc, s));
+        VMB_CHECK_CUDA(cudaFreeAsync(a.part_stat, s));
+    }
 }
 
 #define VMB_DISPATCH_G(G_, FN, T_, ...)                                  \

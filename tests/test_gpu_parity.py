@@ -153,7 +153,8 @@ def test_clamp_disabled_nonpositive_cR_is_domain_error(vm, cuda):
 
 # ------------------------------------------------------------------ online-entropy attention
 @pytest.mark.parametrize("dtype,tol", [(torch.float32, 1e-5), (torch.bfloat16, BF16_TOL)])
-@pytest.mark.parametrize("nq,nk,d", [(128, 128, 128), (100, 300, 128), (300, 1000, 128), (40, 256, 16)])
+@pytest.mark.parametrize("nq,nk,d", [(128, 128, 128), (100, 300, 128), (300, 1000, 128), (40, 256, 16),
+                                    (64, 5000, 64)])  # last: 19-way split-KV on CUDA cores in fp32
 def test_flash_entropy_parity(vm, orc, cuda, dtype, tol, nq, nk, d):
     q = bf16_round(randn((2, nq, d), 1, dtype=np.float32) / np.sqrt(d))
     k = bf16_round(randn((2, nk, d), 2, dtype=np.float32))
