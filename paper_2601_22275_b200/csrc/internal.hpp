@@ -36,6 +36,11 @@ struct Error {
         if (!(cond)) throw ::vmb::Error{VMB_ERR_DOMAIN, std::string("domain error: ") + (msg)}; \
     } while (0)
 
+// Per-call scratch from the device's default stream-ordered pool.  The pool's release
+// threshold is raised once per device, so freed scratch stays mapped for the next call instead
+// of being returned at every synchronisation (which made each call pay for the mapping again).
+void scratch_alloc(void** p, size_t bytes, cudaStream_t s);
+
 extern std::atomic<uint64_t> g_launches;
 inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 

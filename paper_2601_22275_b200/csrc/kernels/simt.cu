@@ -533,10 +533,10 @@ void flash_launch(const SimtFlashArgs& a0, cudaStream_t s) {
     a.nsplit = (int32_t)std::max<int64_t>(1, std::min<int64_t>({(2 * 148 + row_blocks - 1) / row_blocks, 32,
                                                                  a.nk / (8 * KTILE)}));
     if (a.nsplit > 1) {
-        VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.part_acc),
-                                       sizeof(float) * a.nsplit * a.U * a.nq * a.d, s));
-        VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.part_stat),
-                                       sizeof(double) * 3 * a.nsplit * a.U * a.nq, s));
+        scratch_alloc(reinterpret_cast<void**>(&a.part_acc),
+                                       sizeof(float) * a.nsplit * a.U * a.nq * a.d, s);
+        scratch_alloc(reinterpret_cast<void**>(&a.part_stat),
+                                       sizeof(double) * 3 * a.nsplit * a.U * a.nq, s);
     }
     const dim3 grid((unsigned)row_blocks, (unsigned)a.U, (unsigned)a.nsplit);
     const size_t smem = 2 * KTILE * a.d * sizeof(float);

@@ -141,6 +141,24 @@ int attn_impl(bool rstep) {
     return rstep ? r : at;
 }
 
+void scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
+    static std::mutex mu;
+    static std::vector<int> done;
+    int dev = 0;
+    VMB_CHECK_CUDA(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (std::find(done.begin(), done.end(), dev) == done.end()) {
+            cudaMemPool_t pool;
+            VMB_CHECK_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+            uint64_t keep = UINT64_MAX;
+            VMB_CHECK_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+            done.push_back(dev);
+        }
+    }
+    VMB_CHECK_CUDA(cudaMallocAsync(p, bytes, s));
+}
+
 namespace {
 
 constexpr size_t kAlign = 256;
@@ -1161,7 +1179,7 @@ vmb_status vmb_rstep(int64_t units, int64_t m, int64_t b, int64_t d, vmb_dtype d
         const int64_t ud = m * b * d;
         if (!clamp_enabled) {
             int32_t* flag = nullptr;
-            VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&flag), sizeof(int32_t), st));
+            scratch_alloc(reinterpret_cast<void**>(&flag), sizeof(int32_t), st);
             VMB_CHECK_CUDA(cudaMemsetAsync(flag, 0, sizeof(int32_t), st));
             check_clamp_domain(cR, units * m * b, flag, st);
             int32_t h = 0;
@@ -1190,7 +1208,7 @@ vmb_status vmb_rstep(int64_t units, int64_t m, int64_t b, int64_t d, vmb_dtype d
             f2.cl_out = cL;
             f2.max_split = 1;
             int32_t* dummy = nullptr;
-            VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dummy), sizeof(int32_t), st));
+            scratch_alloc(reinterpret_cast<void**>(&dummy), sizeof(int32_t), st);
             f2.status = dummy;
             QRows qv;
             qv.base = aR; qv.B = m * b * d; qv.H = 0; qv.S = b * d; qv.R = d; qv.Hn = 1;
@@ -1199,7 +1217,7 @@ vmb_status vmb_rstep(int64_t units, int64_t m, int64_t b, int64_t d, vmb_dtype d
             return;
         }
         int32_t* dummy = nullptr;
-        VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dummy), sizeof(int32_t), st));
+        scratch_alloc(reinterpret_cast<void**>(&dummy), sizeof(int32_t), st);
         SimtRstepArgs ra{};
         ra.A = internal_view(aR, ud, b * d, d);
         ra.qscale = 1.f;
@@ -1247,7 +1265,7 @@ vmb_status vmb_lstep(int64_t units, int64_t m, int64_t b, int64_t d, vmb_dtype d
             lb.tmY64 = lb.tmAL64;  // unused (ITER)
             float* lse2 = nullptr;
             if (units > 0)
-                VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&lse2), sizeof(float) * units * m * b, st));
+                scratch_alloc(reinterpret_cast<void**>(&lse2), sizeof(float) * units * m * b, st);
             lb.cL = cL;
             lb.lse2 = lse2;
             lb.cR = cR;
@@ -1339,10 +1357,10 @@ vmb_status vmb_flash_entropy_fwd(int64_t units, int64_t nq, int64_t nk, int64_t 
             const int nsplit = attn_plan_splits(nq, nk, units);
             float* part = nullptr;
             int32_t* dummy = nullptr;
-            VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dummy), sizeof(int32_t), st));
+            scratch_alloc(reinterpret_cast<void**>(&dummy), sizeof(int32_t), st);
             if (nsplit > 1) {
-                VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part),
-                                               (size_t)units * nsplit * nq * 130 * sizeof(float), st));
+                scratch_alloc(reinterpret_cast<void**>(&part),
+                                               (size_t)units * nsplit * nq * 130 * sizeof(float), st);
                 f2.part_o = part;
                 f2.part_lse = part + (size_t)units * nsplit * nq * 128;
                 f2.part_ent = part + (size_t)units * nsplit * nq * 129;
@@ -1392,13 +1410,13 @@ vmb_status vmb_flash_entropy_bwd(int64_t units, int64_t nq, int64_t nk, int64_t 
             al32(dv)) {
             void* rowstat = nullptr;
             const size_t rs_bytes = sizeof(float) * 4 * units * flash_bwd_tc_rowstat_rows(nq);
-            VMB_CHECK_CUDA(cudaMallocAsync(&rowstat, rs_bytes, st));
+            scratch_alloc(&rowstat, rs_bytes, st);
             flash_bwd_tc_launch(units, nq, nk, q, k, v, o, dout, lse, ent, dent, entropy_grad, rowstat, dq, dk, dv, st);
             VMB_CHECK_CUDA(cudaFreeAsync(rowstat, st));
             return;
         }
         float* dvec = nullptr;
-        if (units * nq > 0) VMB_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dvec), sizeof(float) * units * nq, st));
+        if (units * nq > 0) scratch_alloc(reinterpret_cast<void**>(&dvec), sizeof(float) * units * nq, st);
         flash_bwd_launch(units, nq, nk, d, dtype == VMB_BF16, q, k, v, o, dout, lse, ent, dent, entropy_grad, dvec, dq,
                          dk, dv, st);
         if (dvec) VMB_CHECK_CUDA(cudaFreeAsync(dvec, st));
