@@ -139,7 +139,9 @@ vmb_status vmb_seq_assemble(const vmb_grid* grid, vmb_dtype dtype, int32_t world
  *    frame, for every unit: q/k/v/o[r] are (units, T*count_r, d), token t*count_r + i, as in
  *    vmb_vmonarch_fwd_seq.  The K/V slabs are all-gathered inside the call by one kernel
  *    per device reading its peers' HBM over NVLink (P2P; peer access is enabled here and
- *    required, VMB_ERR_NCCL otherwise) into workspace[r]; then the slab forward runs.
+ *    required, VMB_ERR_NCCL otherwise) into workspace[r]; then the slab forward runs.  V is
+ *    gathered on a side stream and overlaps the first R/L half-steps (first read by the last
+ *    R half-step).
  *    Default factorization; bf16, d = 128, T <= 128.
  * Stream-ordered on every streams[r]; the call joins all streams (cross-device events)
  * before the gather and after it, so inputs may be rewritten once streams[r] moves on.

@@ -320,7 +320,7 @@ void seq_assemble(const void* gathered, void* full, int64_t units, int64_t T, in
 // v_src[r] (any device with peer access) -> frame-major (units, T*hw, d) at k_dst / v_dst
 void peer_gather(const void* const* k_src, const void* const* v_src, void* k_dst, void* v_dst, int64_t units,
                  int64_t T, int64_t hw, int64_t row_bytes, int world, const int64_t* off, const int64_t* cnt,
-                 cudaStream_t s);
+                 cudaStream_t s, int which = 3);  // which: 1 = K, 2 = V, 3 = both
 
 void selftest_umma(int mode, const void* A, const void* B, float* C, cudaStream_t s);
 

@@ -95,20 +95,21 @@ struct PeerGatherParams {
     int64_t rows_before[kMaxSeqRanks + 1];  // prefix sum of units * T * cnt_p
     int64_t units, T, hw, row_bytes;
     int32_t world;
+    int32_t which;  // 1: K, 2: V, 3: both
 };
 
 __global__ void __launch_bounds__(256) peer_gather_kernel(const __grid_constant__ PeerGatherParams p) {
     const int64_t chunks = p.row_bytes / 16;
     const int64_t rows = p.rows_before[p.world];
-    const int64_t total = 2 * rows * chunks;  // K then V
+    const int64_t total = (p.which == 3 ? 2 : 1) * rows * chunks;  // K then V
     // consecutive threads take consecutive 16-B chunks of one row, so every warp moves whole
     // 256-B rows and the peer reads coalesce into full NVLink packets
     for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
         const int64_t c = idx % chunks;
         int64_t row = idx / chunks;
-        const bool is_v = row >= rows;
-        if (is_v) row -= rows;
+        const bool is_v = p.which == 2 || (p.which == 3 && row >= rows);
+        if (row >= rows) row -= rows;
         int r = 0;
         while (row >= p.rows_before[r + 1]) ++r;
         const int64_t local = row - p.rows_before[r];  // (unit, frame, position) within slab r
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(256) peer_gather_kernel(const __grid_constant_
 
 void peer_gather(const void* const* k_src, const void* const* v_src, void* k_dst, void* v_dst, int64_t units,
                  int64_t T, int64_t hw, int64_t row_bytes, int world, const int64_t* off, const int64_t* cnt,
-                 cudaStream_t s) {
+                 cudaStream_t s, int which) {
     VMB_REQUIRE_DIM(world >= 1 && world <= kMaxSeqRanks, "sequence-sharded world size out of range");
     VMB_REQUIRE_DIM(row_bytes % 16 == 0, "row size must be a multiple of 16 bytes");
     PeerGatherParams p;
@@ -135,6 +136,7 @@ void peer_gather(const void* const* k_src, const void* const* v_src, void* k_dst
     p.hw = hw;
     p.row_bytes = row_bytes;
     p.world = world;
+    p.which = which;
     p.rows_before[0] = 0;
     for (int r = 0; r < kMaxSeqRanks; ++r) {
         const bool in = r < world;
@@ -149,7 +151,7 @@ void peer_gather(const void* const* k_src, const void* const* v_src, void* k_dst
             p.rows_before[r + 1] = p.rows_before[r];
         }
     }
-    const int64_t total = 2 * p.rows_before[world] * (row_bytes / 16);
+    const int64_t total = (which == 3 ? 2 : 1) * p.rows_before[world] * (row_bytes / 16);
     if (total == 0) return;
     int dev = 0, sms = 148;
     VMB_CHECK_CUDA(cudaGetDevice(&dev));

@@ -460,9 +460,11 @@ cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 // in: strides of q; kin: strides of k and v; out: strides of o.  Queries/outputs cover s.bq
 // positions of every frame (s.bq == s.b except in the sequence-sharded mode); keys/values
 // cover all s.b positions.
+// v_ready (optional): V is still arriving (sequence-sharded gather on another stream); the
+// stream waits for it before the first launch that reads V (the last R half-step, with y).
 void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q, const void* k,
              const void* v, void* o, const vmb_strides& in, const vmb_strides& kin, const vmb_strides& out,
-             const Workspace& ws, cudaStream_t st) {
+             const Workspace& ws, cudaStream_t st, cudaEvent_t v_ready = nullptr) {
     const bool bf16 = dt == VMB_BF16;
     const float qscale = (float)(1.0 / std::sqrt((double)(s.d_real > 0 ? s.d_real : s.d)));
     const bool recompute = cfg.recompute_first_frame != 0;
@@ -499,6 +501,7 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
         const CUtensorMap mOcol = user_map(o, out, s, bq, 1, m, bq, 1, lrows);  // O rows j*bq+i: (d, i, j)
         for (int64_t t = 0; t < cfg.iters; ++t) {
             const bool last = t == cfg.iters - 1;
+            if (last && v_ready) VMB_CHECK_CUDA(cudaStreamWaitEvent(st, v_ready, 0));
             TcFaArgs fa{};
             fa.tmQ = t == 0 ? mQrow : mAR;
             fa.tmK = mK;
@@ -1066,14 +1069,23 @@ vmb_status vmb_vmonarch_fwd_multi(int32_t n_dev, const int32_t* devices, vmb_sha
             cnt[r] = parts[r].pos_count;
         }
         const int64_t es = dtype == VMB_BF16 ? 2 : 4;
+        // K is gathered on the call's stream; V, first needed by the last R half-step, on a side
+        // stream per device, so its transfer overlaps the first R and L half-steps
+        std::vector<OverlapStreams*> side(n_dev);
         for (int r = 0; r < n_dev; ++r) {
             const MultiPart& p = parts[r];
             VMB_CHECK_CUDA(cudaSetDevice(devices[r]));
+            side[r] = &overlap_streams();
             uint8_t* base = static_cast<uint8_t*>(workspace[r]);
+            VMB_CHECK_CUDA(cudaEventRecord(side[r]->fork, st[r]));
+            VMB_CHECK_CUDA(cudaStreamWaitEvent(side[r]->chain, side[r]->fork, 0));
             peer_gather(k, v, base + p.fwd_bytes, base + p.fwd_bytes + p.kv_bytes, p.s.U, p.s.T, p.s.hw,
-                        p.s.d * es, n_dev, off.data(), cnt.data(), st[r]);
+                        p.s.d * es, n_dev, off.data(), cnt.data(), st[r], 1);
+            peer_gather(k, v, base + p.fwd_bytes, base + p.fwd_bytes + p.kv_bytes, p.s.U, p.s.T, p.s.hw,
+                        p.s.d * es, n_dev, off.data(), cnt.data(), side[r]->chain, 2);
+            VMB_CHECK_CUDA(cudaEventRecord(side[r]->join, side[r]->chain));
         }
-        join_streams(n_dev, devices, st);  // no device's K/V input is reused before every peer read it
+        join_streams(n_dev, devices, st);  // no device's K input is reused before every peer read it
         for (int r = 0; r < n_dev; ++r) {
             const MultiPart& p = parts[r];
             if (p.s.U == 0) continue;
@@ -1086,7 +1098,12 @@ vmb_status vmb_vmonarch_fwd_multi(int32_t n_dev, const int32_t* devices, vmb_sha
             full.head = p.s.N * p.s.d;
             full.batch = p.s.H * p.s.N * p.s.d;
             forward(p.s, *cfg, dtype, q[r], base + p.fwd_bytes, base + p.fwd_bytes + p.kv_bytes, o[r], local, full,
-                    local, carve(workspace[r], p.s, dtype), st[r]);
+                    local, carve(workspace[r], p.s, dtype), st[r], side[r]->join);
+        }
+        // no device's V input is reused before every peer read it
+        for (int r = 0; r < n_dev; ++r) {
+            VMB_CHECK_CUDA(cudaSetDevice(devices[r]));
+            for (int p2 = 0; p2 < n_dev; ++p2) VMB_CHECK_CUDA(cudaStreamWaitEvent(st[r], side[p2]->join, 0));
         }
     });
 }
