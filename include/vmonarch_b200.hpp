@@ -222,7 +222,7 @@ ResultT flash_entropy_bwd(const MatT& q, const MatT& k, const MatT& v, const Mat
 // ---------------------------------------------------------------- the operator (video.hpp:84-150)
 // Compute precision of the façade.  fp32 (default) is the parity mode: <= 1e-4 of the
 // reference, on CUDA cores.  bf16 rounds the float inputs to bf16 on the host and runs the
-// tcgen05 path (the performance path, <= 2e-2 of the reference; 100-700x faster than fp32 at
+// tcgen05 path (the performance path, <= 2e-2 of the reference; ~200-350x faster than fp32 at
 // the Wan shapes), returning float outputs.  An extra trailing argument, so calls written
 // for the reference signature are unchanged.
 enum class Precision { fp32, bf16 };
