@@ -122,6 +122,14 @@ vmb_status vmb_vmonarch_fwd_seq(const vmb_grid* grid, const vmb_config* cfg, vmb
                                 int64_t pos_begin, int64_t pos_count, const void* q_local,
                                 const void* k_full, const void* v_full, void* o_local,
                                 void* workspace, size_t workspace_bytes, void* stream);
+/* As vmb_vmonarch_fwd_seq, with V still in flight: `v_ready` (a cudaEvent_t passed as void*,
+ * may be NULL) completes when v_full is assembled; the stream waits on it just before the first
+ * launch that reads V (the last R half-step), so the V all-gather overlaps the first R and L
+ * half-steps. */
+vmb_status vmb_vmonarch_fwd_seq_v(const vmb_grid* grid, const vmb_config* cfg, vmb_dtype dtype,
+                                  int64_t pos_begin, int64_t pos_count, const void* q_local,
+                                  const void* k_full, const void* v_full, void* o_local,
+                                  void* workspace, size_t workspace_bytes, void* stream, void* v_ready);
 /* gathered: `world` blocks of (units, T, slab_max, d) (slab r padded to slab_max rows) ->
  * full (units, T*h*w, d); rank r's rows land at positions [pos_begin[r], +pos_count[r]). */
 vmb_status vmb_seq_assemble(const vmb_grid* grid, vmb_dtype dtype, int32_t world, const int64_t* pos_begin,

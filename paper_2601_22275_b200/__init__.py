@@ -112,6 +112,8 @@ _vmb_launches = _sig("vmb_kernel_launch_count", [], C.c_uint64)
 _vmb_ws_size_seq = _sig("vmb_workspace_size_seq", [C.POINTER(_Grid), C.POINTER(_Cfg), C.c_int, _I64], C.c_size_t)
 _vmb_fwd_seq = _sig("vmb_vmonarch_fwd_seq", [C.POINTER(_Grid), C.POINTER(_Cfg), C.c_int, _I64, _I64, _P, _P, _P, _P,
                                              _P, C.c_size_t, _P])
+_vmb_fwd_seq_v = _sig("vmb_vmonarch_fwd_seq_v", [C.POINTER(_Grid), C.POINTER(_Cfg), C.c_int, _I64, _I64, _P, _P, _P,
+                                                 _P, _P, C.c_size_t, _P, _P])
 _vmb_seq_assemble = _sig("vmb_seq_assemble", [C.POINTER(_Grid), C.c_int, _I32, _P, _P, _I64, _P, _P, _P])
 _vmb_shard_range = _sig("vmb_shard_range", [_I64, _I32, _I32, C.POINTER(_I64), C.POINTER(_I64)], None)
 _vmb_ws_size_multi = _sig("vmb_workspace_size_multi", [_I32, _I32, C.c_int, C.POINTER(_Grid), C.POINTER(_Cfg),
@@ -403,7 +405,8 @@ def vmonarch_attention_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, g
 # ----------------------------------------------------------------------------- sequence-sharded mode
 def vmonarch_attention_slab(q_local: torch.Tensor, k_full: torch.Tensor, v_full: torch.Tensor, grid: TokenGrid,
                             pos_begin: int, pos_count: int, cfg: VMonarchConfig = VMonarchConfig(),
-                            out: Optional[torch.Tensor] = None, check: bool = True) -> torch.Tensor:
+                            out: Optional[torch.Tensor] = None, check: bool = True,
+                            v_ready: Optional[torch.cuda.Event] = None) -> torch.Tensor:
     """The forward for the spatial slab [pos_begin, pos_begin + pos_count) of every frame
     (SURVEY §8e): q_local / output (units, T * pos_count, d) with local token
     t * pos_count + (position - pos_begin); k_full, v_full (units, N, d).  Slab outputs of all
@@ -428,8 +431,9 @@ def vmonarch_attention_slab(q_local: torch.Tensor, k_full: torch.Tensor, v_full:
         _WS_CACHE.clear()
         _WS_CACHE[key] = ws
     st = _stream()
-    _check(_vmb_fwd_seq(C.byref(g), C.byref(c), dt, pos_begin, pos_count, _ptr(q_local), _ptr(k_full), _ptr(v_full),
-                        _ptr(out), _ptr(ws), ws.numel(), st))
+    ev = C.c_void_p(v_ready.cuda_event) if v_ready is not None else None
+    _check(_vmb_fwd_seq_v(C.byref(g), C.byref(c), dt, pos_begin, pos_count, _ptr(q_local), _ptr(k_full), _ptr(v_full),
+                          _ptr(out), _ptr(ws), ws.numel(), st, ev))
     if check:
         _check(_vmb_ws_status(_ptr(ws), st))
     return out

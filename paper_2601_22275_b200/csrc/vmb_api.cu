@@ -892,6 +892,13 @@ size_t vmb_workspace_size_seq(const vmb_grid* grid, const vmb_config* cfg, vmb_d
 vmb_status vmb_vmonarch_fwd_seq(const vmb_grid* grid, const vmb_config* cfg, vmb_dtype dtype, int64_t pos_begin,
                                 int64_t pos_count, const void* q_local, const void* k_full, const void* v_full,
                                 void* o_local, void* workspace, size_t ws_bytes, void* stream) {
+    return vmb_vmonarch_fwd_seq_v(grid, cfg, dtype, pos_begin, pos_count, q_local, k_full, v_full, o_local, workspace,
+                                  ws_bytes, stream, nullptr);
+}
+
+vmb_status vmb_vmonarch_fwd_seq_v(const vmb_grid* grid, const vmb_config* cfg, vmb_dtype dtype, int64_t pos_begin,
+                                  int64_t pos_count, const void* q_local, const void* k_full, const void* v_full,
+                                  void* o_local, void* workspace, size_t ws_bytes, void* stream, void* v_ready) {
     return guarded([&] {
         const Shape s = seq_shape(grid, cfg, pos_begin, pos_count);
         VMB_REQUIRE_DIM(dtype == VMB_BF16 && s.d == 128 && s.m <= 128,
@@ -905,7 +912,8 @@ vmb_status vmb_vmonarch_fwd_seq(const vmb_grid* grid, const vmb_config* cfg, vmb
         local.batch = s.H * s.Nq * s.d;
         full.head = s.N * s.d;
         full.batch = s.H * s.N * s.d;
-        forward(s, *cfg, dtype, q_local, k_full, v_full, o_local, local, full, local, ws, as_stream(stream));
+        forward(s, *cfg, dtype, q_local, k_full, v_full, o_local, local, full, local, ws, as_stream(stream),
+                static_cast<cudaEvent_t>(v_ready));
     });
 }
 

@@ -81,13 +81,27 @@ def vmonarch_attention_seq(q_local, k_local, v_local, grid, cfg=None, group=None
 
     import paper_2601_22275_b200 as vm
 
+    import torch
+
     cfg = cfg or vm.VMonarchConfig()
     rank = dist.get_rank(group)
+    main = torch.cuda.current_stream(q_local.device)
+    # K first, on the caller's stream: the first R half-step needs it
     kg, parts, _ = gather_slabs(k_local, grid, group)
-    vg, _, _ = gather_slabs(v_local, grid, group)
     begins = [a for a, _ in parts]
     counts = [c for _, c in parts]
     k_full = vm.seq_assemble(kg, grid, begins, counts)
-    v_full = vm.seq_assemble(vg, grid, begins, counts)
+    # V on a side stream: first read by the last R half-step, so its all-gather overlaps the
+    # first R and L half-steps (every rank issues K then V: the same collective order)
+    side = torch.cuda.Stream(device=q_local.device)
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        vg, _, _ = gather_slabs(v_local, grid, group)
+        v_full = vm.seq_assemble(vg, grid, begins, counts)
+        v_ready = torch.cuda.Event()
+        v_ready.record(side)
     b0, cnt = parts[rank]
-    return vm.vmonarch_attention_slab(q_local, k_full, v_full, grid, b0, cnt, cfg, check=False)
+    out = vm.vmonarch_attention_slab(q_local, k_full, v_full, grid, b0, cnt, cfg, check=False, v_ready=v_ready)
+    main.wait_stream(side)
+    v_full.record_stream(main)  # allocated on the side stream, read on the main one
+    return out

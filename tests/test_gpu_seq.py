@@ -70,3 +70,39 @@ def test_seq_slab_validation(vm, cuda):
     with pytest.raises(vm.DimensionError):
         vm.vmonarch_attention_slab(torch.zeros((1, 4 * 10, 128), device=cuda, dtype=torch.float32), x.float(),
                                    x.float(), grid, 0, 10)
+
+
+NCCL_SCRIPT = r"""
+import os, sys, json, socket
+import torch, torch.distributed as dist
+sys.path.insert(0, %(root)r)
+s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
+import paper_2601_22275_b200 as vm
+from paper_2601_22275_b200.dist import vmonarch_attention_seq, local_slab
+grid = vm.TokenGrid(6, 10, 26, 128, 2, 1)
+g = torch.Generator(device="cuda").manual_seed(3)
+q, k, v = (torch.randn((2, grid.tokens(), 128), generator=g, device="cuda").bfloat16() for _ in range(3))
+full = vm.vmonarch_attention(q, k, v, grid)
+sl = lambda x: local_slab(x, grid, 0, grid.h * grid.w)
+out = vmonarch_attention_seq(sl(q), sl(k), sl(v), grid)
+torch.cuda.synchronize()
+print(json.dumps({"equal": bool(torch.equal(out, sl(full)))}))
+dist.destroy_process_group()
+"""
+
+
+def test_dist_seq_path_one_rank_nccl(cuda):
+    # the process-per-GPU path end to end on a 1-rank NCCL group: K all-gather on the caller's
+    # stream, V all-gather + assembly on a side stream, the forward waiting on the V-ready event
+    import json as _json
+    import os as _os
+    import subprocess
+    import sys as _sys
+    root = _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__)))
+    r = subprocess.run([_sys.executable, "-c", NCCL_SCRIPT % {"root": root}], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert _json.loads(r.stdout.strip().splitlines()[-1])["equal"]
