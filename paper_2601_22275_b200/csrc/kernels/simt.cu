@@ -2,7 +2,7 @@
 //
 // These serve (1) the fp32 parity mode (VMB_F32: fp32 storage, fp32 dot products,
 // double row sums / entropy exactly where the reference uses double) and (2) any
-// bf16 shape the tcgen05 kernels do not cover (d != 128, m > 128).  They are
+// bf16 shape the tcgen05 kernels do not cover (d > 128).  They are
 // GPU kernels, not a CPU fallback.
 //
 // Thread mapping: G threads cooperate on one row, each owning 32 consecutive

@@ -7,7 +7,7 @@
 //     R half-step      fa_tc <1,1>  (last iteration: <2,2>, y = R V fused)
 //     L half-step      lstep_tc ITER (last iteration: FINAL -> O, permutation folded)
 //   first-frame recompute  fa_tc <2,1> over Q[0:hw] x all keys -> O[0:hw)
-// Shapes outside the tcgen05 kernels' envelope (fp32 parity mode, d != 128, m > 128)
+// Shapes outside the tcgen05 kernels' envelope (fp32 parity mode, d > 128)
 // run the same plan on the CUDA-core kernels in kernels/simt.cu.
 #include <cuda_bf16.h>
 
