@@ -4,11 +4,13 @@
 // Launch plan of vmb_vmonarch_fwd (reference: video.hpp:84-150 + monarch.hpp:155-193),
 // all batch*head units batched into every launch:
 //   for t in [0, iters):
-//     R half-step      fa_tc <1,1>  (last iteration: <2,2>, y = R V fused)
-//     L half-step      lstep_tc ITER (last iteration: FINAL -> O, permutation folded)
-//   first-frame recompute  fa_tc <2,1> over Q[0:hw] x all keys -> O[0:hw)
-// Shapes outside the tcgen05 kernels' envelope (fp32 parity mode, d > 128)
-// run the same plan on the CUDA-core kernels in kernels/simt.cu.
+//     R half-step      fa2 (last iteration: persistent fa4 <2,2>, y = R V fused)
+//     L half-step      lstep_tc ITER (last iteration: FINAL -> O, permutation folded);
+//                      m > 128: the lstep_big passes
+//   first-frame recompute  fa3 split-KV over Q[0:hw] x all keys + combine -> O[0:hw)
+// bf16 head dims below 128 run the same plan on zero-padded copies; shapes outside the
+// tcgen05 kernels' envelope (fp32 parity mode, d > 128) run it on the CUDA-core kernels in
+// kernels/simt.cu.
 #include <cuda_bf16.h>
 
 #include <algorithm>
