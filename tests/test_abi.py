@@ -157,3 +157,20 @@ def test_torch_op_fake_kernel_on_cpu(vm):
         q, k, v = qkv.unbind(2)
         o = torch.ops.vmb.vmonarch_attention(q, k, v, 4, 8, 16)
         assert o.shape == (2, 512, 2, 128) and o.dtype == torch.bfloat16
+
+
+def test_plain_c_caller(tmp_path):
+    """include/vmb.h is a plain C ABI: a C11 program (-Wall -Werror) links libvmb and calls it."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_2601_22275_b200")
+    exe = str(tmp_path / "c_abi_example")
+    cc = subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-I", os.path.join(root, "include"),
+                         os.path.join(root, "tests", "c_abi_example.c"), "-L", libdir, "-lvmb", f"-Wl,-rpath,{libdir}",
+                         "-L/usr/local/cuda/lib64", "-lcudart", "-o", exe], capture_output=True, text=True)
+    assert cc.returncode == 0, cc.stderr
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0 and r.stdout.startswith("ok"), (r.returncode, r.stdout, r.stderr)
