@@ -26,8 +26,9 @@
 // running max grows by more than 8).  The entropy of the R-step is not accumulated per
 // element: with value = key, sum_l R_l s_l = <q, sum_l R_l k_l> = <q, O> / l, so
 //   sum_l R ln R = ln2 * (scale2 * <q, O> / l - lse2)            (monarch.hpp:93-98)
-// is one 128-term dot product in the epilogue.  A quarter of the exponentials run as a
-// degree-3 polynomial on the FMA pipe (MUFU ex2 is 16/clk/SM, the softmax's binding unit).
+// is one 128-term dot product in the epilogue.  Exponentials run on MUFU; the FMA-pipe
+// polynomial for one pair in VMB_EMU_PERIOD is compiled in but off by default (measured: MUFU
+// is not the binding unit, profiles/r1_fa_variants.md).
 #include <cuda_bf16.h>
 
 #include <algorithm>

@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa6_kernel(const __grid_constant_
                     rescale = true;
                 }
             }
-            // x' - m on the packed FMA pipe, 2^(x' - m): MUFU for 7 of 8 pairs, FMA-pipe
+            // x' - m on the packed FMA pipe, 2^(x' - m) on MUFU (VMB_EMU_PERIOD: FMA-pipe polynomial, off),
             // polynomial for the 8th; row sum in packed adds; P -> TMEM as bf16
             const uint64_t negm2 = pk2(-m_run, -m_run);
             const uint64_t* s2 = reinterpret_cast<const uint64_t*>(sr);

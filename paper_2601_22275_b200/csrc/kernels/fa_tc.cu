@@ -349,9 +349,9 @@ __global__ void __launch_bounds__(kThreads, 1) fa_tc_kernel(const __grid_constan
                     rescale = true;
                 }
             }
-            // x' - m on the packed FMA pipe; 2^(x' - m) on MUFU for 7 of 8 pairs and the FMA-pipe
-            // polynomial for the 8th (MUFU, 16 ex2/clk/SM, binds the softmax: SURVEY §7 hard
-            // part 4); packed row sums; P -> TMEM as bf16
+            // x' - m on the packed FMA pipe; 2^(x' - m) on MUFU (VMB_EMU_PERIOD moves one pair in
+            // that many to the FMA-pipe polynomial; off by default, profiles/r1_fa_variants.md);
+            // packed row sums; P -> TMEM as bf16
             const uint64_t negm2 = pk2(-m_run, -m_run);
             const uint64_t* s2 = reinterpret_cast<const uint64_t*>(sr);
             uint64_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
