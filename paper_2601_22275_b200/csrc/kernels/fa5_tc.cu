@@ -372,8 +372,8 @@ __global__ void __launch_bounds__(kThreads, 1) fa5_kernel(const __grid_constant_
                     rescale = true;
                 }
             }
-            // x' - m on the packed FMA pipe, 2^(x' - m) on MUFU (VMB_EMU_PERIOD: FMA-pipe polynomial, off),
-            // polynomial for the 8th; row sum in packed adds; P -> TMEM as bf16
+            // x' - m on the packed FMA pipe, 2^(x' - m) on MUFU (VMB_EMU_PERIOD: FMA-pipe polynomial,
+            // off by default); row sum in packed adds; P -> TMEM as bf16
             const uint64_t negm2 = pk2(-m_run, -m_run);
             const uint64_t* s2 = reinterpret_cast<const uint64_t*>(sr);
             uint64_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
