@@ -460,18 +460,31 @@ __global__ void __launch_bounds__(256) fa2_combine_kernel(const Tc2Args a) {
     if (useg >= a.n_useg) return;
     const int u = (int)(useg / a.nseg), seg = (int)(useg % a.nseg);
     const float* lse = a.part_lse + (useg * a.nsplit) * rows + r;
+    // all split statistics and partial rows are loaded up front (independent loads in flight,
+    // registers: nsplit <= kTc2MaxSplit), then reduced in split order
+    float ls[kTc2MaxSplit];
+    float4 pv[kTc2MaxSplit];
     float mx = -INFINITY;
-    for (int s = 0; s < a.nsplit; ++s) mx = fmaxf(mx, lse[(int64_t)s * rows]);
+#pragma unroll
+    for (int s = 0; s < kTc2MaxSplit; ++s) {
+        ls[s] = s < a.nsplit ? lse[(int64_t)s * rows] : -INFINITY;
+        pv[s] = s < a.nsplit
+                    ? reinterpret_cast<const float4*>(a.part_o + ((useg * a.nsplit + s) * rows + r) * 128)[lane]
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int s = 0; s < kTc2MaxSplit; ++s) mx = fmaxf(mx, ls[s]);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     float wsum = 0.f;
-    for (int s = 0; s < a.nsplit; ++s) {
-        const float w = __expf(lse[(int64_t)s * rows] - mx);
+#pragma unroll
+    for (int s = 0; s < kTc2MaxSplit; ++s) {
+        if (s >= a.nsplit) break;
+        const float w = __expf(ls[s] - mx);
         wsum += w;
-        const float4 v = reinterpret_cast<const float4*>(a.part_o + ((useg * a.nsplit + s) * rows + r) * 128)[lane];
-        acc.x = fmaf(w, v.x, acc.x);
-        acc.y = fmaf(w, v.y, acc.y);
-        acc.z = fmaf(w, v.z, acc.z);
-        acc.w = fmaf(w, v.w, acc.w);
+        acc.x = fmaf(w, pv[s].x, acc.x);
+        acc.y = fmaf(w, pv[s].y, acc.y);
+        acc.z = fmaf(w, pv[s].z, acc.z);
+        acc.w = fmaf(w, pv[s].w, acc.w);
     }
     const float inv = 1.f / wsum;
     if (a.ent_out && lane == 0) {
