@@ -26,6 +26,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 import os
+from collections import OrderedDict
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence, Tuple
 
@@ -37,6 +38,7 @@ __all__ = [
     "factorize", "flops_estimate", "make_perm", "preset_grid", "export_factors", "lib",
     "kernel_launch_count", "LIB_PATH", "vmonarch_attention_slab", "seq_assemble", "vmonarch_attention_host",
     "flash_entropy_bwd", "vmonarch_attention_multi", "shard_range", "SHARD_MODES", "CudaError",
+    "workspace_size",
 ]
 
 LIB_PATH = os.environ.get("VMB_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libvmb.so")
@@ -229,8 +231,16 @@ def _dtype_code(t: torch.Tensor) -> int:
     raise DimensionError(f"dimension error: unsupported dtype {t.dtype} (float32 or bfloat16)")
 
 
-def _stream() -> C.c_void_p:
-    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+def _stream(device: Optional[torch.device] = None) -> C.c_void_p:
+    """The current stream of `device` (of the current device when None)."""
+    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _call(device: torch.device, fn, *args):
+    """One ABI call ordered on `device`'s current stream (passed last), with that device
+    current for its duration."""
+    with torch.cuda.device(device):
+        _check(fn(*args, _stream(device)))
 
 
 def _ptr(t: Optional[torch.Tensor]):
@@ -264,27 +274,64 @@ def _bhsd_strides(t: torch.Tensor, grid: TokenGrid) -> _Strides:
     raise DimensionError("dimension error: Q/K/V must be 3-D (units, N, d) or 4-D (B, H, N, d)")
 
 
-_WS_CACHE: dict = {}
+class _WorkspaceCache:
+    """Workspaces keyed by (device, stream, kind).
+
+    The ABI's rule is one workspace per concurrent call (vmb.h).  A buffer here is only ever
+    handed to calls on the stream it is keyed by, so calls on different streams (CFG
+    branches, the host pipeline's compute stream, user streams) never share one, and a buffer
+    that is replaced or evicted was last used on its own allocation stream -- the caching
+    allocator reuses it in that stream's order, so dropping it needs no record_stream.  Under
+    CUDA-graph capture a fresh workspace comes from the capture's pool on every call."""
+
+    def __init__(self, max_entries: int = 8):
+        self._d: "OrderedDict" = OrderedDict()
+        self.max_entries = max_entries
+
+    def get(self, device: torch.device, stream: torch.cuda.Stream, kind: str, nbytes: int) -> torch.Tensor:
+        if torch.cuda.is_current_stream_capturing():
+            return torch.empty(nbytes, dtype=torch.uint8, device=device)
+        key = (device.index, stream.cuda_stream, kind)
+        ws = self._d.get(key)
+        if ws is None or ws.numel() < nbytes:
+            self._d.pop(key, None)
+            ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+            self._d[key] = ws
+        self._d.move_to_end(key)
+        while len(self._d) > self.max_entries:
+            self._d.popitem(last=False)
+        return ws
+
+    def clear(self):
+        self._d.clear()
 
 
-def _workspace(grid: TokenGrid, cfg: VMonarchConfig, dt: int, device) -> torch.Tensor:
+_WS_CACHE = _WorkspaceCache()
+
+
+def _workspace(grid: TokenGrid, cfg: VMonarchConfig, dt: int, device: torch.device,
+               stream: torch.cuda.Stream) -> torch.Tensor:
     g, c = grid._c(), cfg._c()
     nbytes = int(_vmb_ws_size(C.byref(g), C.byref(c), dt))
     if nbytes == 0:
         _check(1)
-    key = (device, nbytes)
-    ws = _WS_CACHE.get(key)
-    if ws is None:
-        ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
-        _WS_CACHE.clear()
-        _WS_CACHE[key] = ws
-    return ws
+    return _WS_CACHE.get(device, stream, "fwd", nbytes)
+
+
+def _check_out(out: torch.Tensor, q: torch.Tensor):
+    """A caller-supplied output must match q's dtype and device: the ABI writes it with q's
+    element size (vmb.h), so a mismatch would write outside the buffer."""
+    if out.dtype != q.dtype:
+        raise DimensionError(f"dimension error: out dtype {out.dtype} != q dtype {q.dtype}")
+    if out.device != q.device:
+        raise DimensionError(f"dimension error: out on {out.device}, q on {q.device}")
 
 
 # ----------------------------------------------------------------------------- the operator
 def vmonarch_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, grid: TokenGrid,
                        cfg: VMonarchConfig = VMonarchConfig(), out: Optional[torch.Tensor] = None,
-                       factors_out: Optional[list] = None, check: bool = True) -> torch.Tensor:
+                       factors_out: Optional[list] = None, check: bool = True,
+                       workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
     """video.hpp:84-150 on the GPU.
 
     q, k, v: CUDA tensors (units, N, d) [unit u = b*H + h], or (B, H, N, d) views (BSHD
@@ -293,11 +340,16 @@ def vmonarch_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, grid: 
     ``factors_out``: if a list, receives per-unit (L (b,m,m), R (m,b,b)) fp32 tensors (small N).
     ``check``: synchronise and raise DomainError for device-detected domain errors
     (non-finite Q, monarch.hpp:44).  Set False inside timed loops.
+    ``workspace``: optional caller-owned uint8 scratch of >= workspace_size(grid, cfg) bytes;
+    by default one is cached per (device, stream).  The call is ordered on q.device's current
+    stream.
     """
     _require_cuda(q, k, v, out)
     dt = _dtype_code(q)
     if k.dtype != q.dtype or v.dtype != q.dtype:
         raise DimensionError("dimension error: Q, K, V must share dtype")
+    if k.device != q.device or v.device != q.device:
+        raise DimensionError("dimension error: Q, K, V must be on one device")
     sq, sk, sv = _bhsd_strides(q, grid), _bhsd_strides(k, grid), _bhsd_strides(v, grid)
     if (sk.batch, sk.head, sk.token) != (sq.batch, sq.head, sq.token) or \
             (sv.batch, sv.head, sv.token) != (sq.batch, sq.head, sq.token):
@@ -309,24 +361,41 @@ def vmonarch_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, grid: 
         sq = _bhsd_strides(q, grid)
     if out is None:
         out = torch.empty(q.shape, dtype=q.dtype, device=q.device)
+    _check_out(out, q)
     so = _bhsd_strides(out, grid)
-    ws = _workspace(grid, cfg, dt, q.device)
-    g, c = grid._c(), cfg._c()
-    st = _stream()
-    _check(_vmb_fwd(C.byref(g), C.byref(c), dt, _ptr(q), _ptr(k), _ptr(v), _ptr(out), C.byref(sq),
-                    C.byref(so), _ptr(ws), ws.numel(), st))
-    if check or factors_out is not None:
-        _check(_vmb_ws_status(_ptr(ws), st))
-    if factors_out is not None:
-        m, b = factorize(grid, cfg)
-        U = grid.units()
-        L = torch.empty((U, b, m, m), dtype=torch.float32, device=q.device)
-        R = torch.empty((U, m, b, b), dtype=torch.float32, device=q.device)
-        _check(_vmb_export(C.byref(g), C.byref(c), dt, _ptr(q), _ptr(k), C.byref(sq), _ptr(ws), _ptr(L),
-                           _ptr(R), st))
-        factors_out.clear()
-        factors_out.extend((L[u], R[u]) for u in range(U))
+    dev = q.device
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev)
+        ws = workspace if workspace is not None else _workspace(grid, cfg, dt, dev, stream)
+        g, c = grid._c(), cfg._c()
+        need = int(_vmb_ws_size(C.byref(g), C.byref(c), dt))
+        if ws.device != dev or ws.dtype != torch.uint8 or not ws.is_contiguous() or ws.numel() < need:
+            raise DimensionError(f"dimension error: workspace must be a contiguous uint8 tensor of >= {need} "
+                                 f"bytes on {dev}")
+        st = C.c_void_p(stream.cuda_stream)
+        _check(_vmb_fwd(C.byref(g), C.byref(c), dt, _ptr(q), _ptr(k), _ptr(v), _ptr(out), C.byref(sq),
+                        C.byref(so), _ptr(ws), ws.numel(), st))
+        if check or factors_out is not None:
+            _check(_vmb_ws_status(_ptr(ws), st))
+        if factors_out is not None:
+            m, b = factorize(grid, cfg)
+            U = grid.units()
+            L = torch.empty((U, b, m, m), dtype=torch.float32, device=dev)
+            R = torch.empty((U, m, b, b), dtype=torch.float32, device=dev)
+            _check(_vmb_export(C.byref(g), C.byref(c), dt, _ptr(q), _ptr(k), C.byref(sq), _ptr(ws), _ptr(L),
+                               _ptr(R), st))
+            factors_out.clear()
+            factors_out.extend((L[u], R[u]) for u in range(U))
     return out
+
+
+def workspace_size(grid: TokenGrid, cfg: VMonarchConfig = VMonarchConfig(), dtype=torch.bfloat16) -> int:
+    """Bytes of scratch one vmonarch_attention call needs (vmb_workspace_size)."""
+    g, c = grid._c(), cfg._c()
+    n = int(_vmb_ws_size(C.byref(g), C.byref(c), VMB_BF16 if dtype == torch.bfloat16 else VMB_F32))
+    if n == 0:
+        _check(1)
+    return n
 
 
 # ----------------------------------------------------------------------------- host-buffer pipeline
@@ -347,11 +416,16 @@ _PIPE: dict = {}
 
 def vmonarch_attention_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, grid: TokenGrid,
                             cfg: VMonarchConfig = VMonarchConfig(), out: Optional[torch.Tensor] = None,
-                            chunk_units: int = 8, device=None) -> torch.Tensor:
+                            chunk_units: int = 8, device=None, sync: bool = True) -> torch.Tensor:
     """video.hpp:84-150 for HOST tensors (units, N, d): batch*head units are independent
     (video.hpp:131-148), so chunks of units stream through the device -- the H2D copy of chunk
     c+1, the forward of chunk c and the D2H copy of chunk c-1 run on three CUDA streams.
-    Inputs should be pinned for the copies to overlap.  Returns the host output."""
+    Inputs should be pinned for the copies to overlap.  Returns the host output.
+
+    Like the reference operator, the call returns finished results (``sync=True``: the host
+    waits for the last D2H copy).  With ``sync=False`` it returns as soon as the work is
+    queued: ``out`` is complete once the device's current stream reaches this point, and the
+    inputs must stay unchanged until then (the H2D copies read them asynchronously)."""
     if q.is_cuda or k.is_cuda or v.is_cuda:
         raise DimensionError("dimension error: vmonarch_attention_host takes host tensors")
     device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -365,6 +439,8 @@ def vmonarch_attention_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, g
     key = (tuple(q.shape), q.dtype, device, chunk, nbuf)
     pipe = _PIPE.get(key)
     if pipe is None:
+        for old in _PIPE.values():  # an unsynchronised call may still use the old buffers
+            old.d2h.synchronize()
         _PIPE.clear()
         pipe = _PIPE[key] = _HostPipeline(tuple(q.shape), q.dtype, device, chunk, nbuf)
     cur = torch.cuda.current_stream(device)
@@ -399,6 +475,8 @@ def vmonarch_attention_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, g
             ev_free[slot] = torch.cuda.Event()
             ev_free[slot].record(d2h)
     cur.wait_stream(d2h)
+    if sync:
+        d2h.synchronize()
     return out
 
 
@@ -417,25 +495,30 @@ def vmonarch_attention_slab(q_local: torch.Tensor, k_full: torch.Tensor, v_full:
     nl = grid.t_frames * pos_count
     if tuple(q_local.shape) != (U, nl, d) or tuple(k_full.shape) != (U, n, d) or tuple(v_full.shape) != (U, n, d):
         raise DimensionError(f"dimension error: expected q_local ({U}, {nl}, {d}) and k/v ({U}, {n}, {d})")
+    if k_full.dtype != q_local.dtype or v_full.dtype != q_local.dtype:
+        raise DimensionError("dimension error: Q, K, V must share dtype")
+    if k_full.device != q_local.device or v_full.device != q_local.device:
+        raise DimensionError("dimension error: Q, K, V must be on one device")
     q_local, k_full, v_full = q_local.contiguous(), k_full.contiguous(), v_full.contiguous()
     if out is None:
         out = torch.empty_like(q_local)
+    _check_out(out, q_local)
+    if tuple(out.shape) != (U, nl, d) or not out.is_contiguous():
+        raise DimensionError(f"dimension error: out must be a contiguous ({U}, {nl}, {d}) tensor")
     g, c = grid._c(), cfg._c()
     nbytes = int(_vmb_ws_size_seq(C.byref(g), C.byref(c), dt, pos_count))
     if nbytes == 0:
         _check(1)
-    key = (q_local.device, nbytes, "seq")
-    ws = _WS_CACHE.get(key)
-    if ws is None:
-        ws = torch.empty(nbytes, dtype=torch.uint8, device=q_local.device)
-        _WS_CACHE.clear()
-        _WS_CACHE[key] = ws
-    st = _stream()
-    ev = C.c_void_p(v_ready.cuda_event) if v_ready is not None else None
-    _check(_vmb_fwd_seq_v(C.byref(g), C.byref(c), dt, pos_begin, pos_count, _ptr(q_local), _ptr(k_full), _ptr(v_full),
-                          _ptr(out), _ptr(ws), ws.numel(), st, ev))
-    if check:
-        _check(_vmb_ws_status(_ptr(ws), st))
+    dev = q_local.device
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev)
+        ws = _WS_CACHE.get(dev, stream, "seq", nbytes)
+        st = C.c_void_p(stream.cuda_stream)
+        ev = C.c_void_p(v_ready.cuda_event) if v_ready is not None else None
+        _check(_vmb_fwd_seq_v(C.byref(g), C.byref(c), dt, pos_begin, pos_count, _ptr(q_local), _ptr(k_full),
+                              _ptr(v_full), _ptr(out), _ptr(ws), ws.numel(), st, ev))
+        if check:
+            _check(_vmb_ws_status(_ptr(ws), st))
     return out
 
 
@@ -449,8 +532,17 @@ def seq_assemble(gathered: torch.Tensor, grid: TokenGrid, pos_begin: Sequence[in
     b = (C.c_int64 * world)(*pos_begin)
     cn = (C.c_int64 * world)(*pos_count)
     g = grid._c()
-    _check(_vmb_seq_assemble(C.byref(g), _dtype_code(gathered), world, C.addressof(b), C.addressof(cn), smax,
-                             _ptr(gathered.contiguous()), _ptr(out), _stream()))
+    if out.dtype != gathered.dtype or out.device != gathered.device or not out.is_contiguous() or \
+            tuple(out.shape) != (U, grid.tokens(), d):
+        raise DimensionError(f"dimension error: out must be a contiguous ({U}, {grid.tokens()}, {d}) tensor "
+                             "of the gathered dtype and device")
+    if len(pos_begin) != world or len(pos_count) != world or T != grid.t_frames or \
+            any(c_ > smax for c_ in pos_count) or sum(pos_count) != grid.h * grid.w:
+        raise DimensionError("dimension error: slab partition does not match the gathered tensor")
+    gathered = gathered.contiguous()
+    with torch.cuda.device(gathered.device):
+        _check(_vmb_seq_assemble(C.byref(g), _dtype_code(gathered), world, C.addressof(b), C.addressof(cn), smax,
+                                 _ptr(gathered), _ptr(out), _stream(gathered.device)))
     return out
 
 
@@ -482,6 +574,19 @@ def vmonarch_attention_multi(qs: Sequence[torch.Tensor], ks: Sequence[torch.Tens
         raise DimensionError(f"dimension error: unknown shard mode {mode!r}")
     dt = _dtype_code(qs[0])
     g, c = grid._c(), cfg._c()
+    U, N, d, T = grid.units(), grid.tokens(), grid.head_dim, grid.t_frames
+    for r in range(n):
+        if mode == "heads":
+            want = (shard_range(U, n, r)[1], N, d)
+        else:
+            want = (U, T * shard_range(grid.h * grid.w, n, r)[1], d)
+        for name, x in (("q", qs[r]), ("k", ks[r]), ("v", vs[r])):
+            if tuple(x.shape) != want:
+                raise DimensionError(f"dimension error: part {r} {name} has shape {tuple(x.shape)}, expected {want}")
+            if x.dtype != qs[0].dtype:
+                raise DimensionError(f"dimension error: part {r} {name} dtype {x.dtype} != {qs[0].dtype}")
+            if x.device != qs[r].device:
+                raise DimensionError(f"dimension error: part {r} q/k/v must share one device")
     qs = [x.contiguous() for x in qs]
     ks = [x.contiguous() for x in ks]
     vs = [x.contiguous() for x in vs]
@@ -514,11 +619,12 @@ def export_factors(q, k, grid, cfg, dtype_code):
     U = grid.units()
     L = torch.empty((U, b, m, m), dtype=torch.float32, device=q.device)
     R = torch.empty((U, m, b, b), dtype=torch.float32, device=q.device)
-    ws = _workspace(grid, cfg, dtype_code, q.device)
+    stream = torch.cuda.current_stream(q.device)
+    ws = _workspace(grid, cfg, dtype_code, q.device, stream)
     g, c = grid._c(), cfg._c()
     sq = _bhsd_strides(q, grid)
-    _check(_vmb_export(C.byref(g), C.byref(c), dtype_code, _ptr(q), _ptr(k), C.byref(sq), _ptr(ws),
-                       _ptr(L), _ptr(R), _stream()))
+    _call(q.device, _vmb_export, C.byref(g), C.byref(c), dtype_code, _ptr(q), _ptr(k), C.byref(sq), _ptr(ws),
+          _ptr(L), _ptr(R))
     return L, R
 
 
@@ -534,8 +640,8 @@ def r_update(aR: torch.Tensor, cR: torch.Tensor, Kb: torch.Tensor, clamp_min: fl
     aL = torch.empty((U, b, m, d), dtype=aR.dtype, device=aR.device)
     cL = torch.empty((U, b, m), dtype=torch.float32, device=aR.device)
     R = torch.empty((U, m, b, b), dtype=torch.float32, device=aR.device) if want_R else None
-    _check(_vmb_rstep(U, m, b, d, dt, _ptr(aR), _ptr(cR), _ptr(Kb), clamp_min, int(clamp_enabled), _ptr(aL),
-                      _ptr(cL), _ptr(R), _stream()))
+    _call(aR.device, _vmb_rstep, U, m, b, d, dt, _ptr(aR), _ptr(cR), _ptr(Kb), clamp_min, int(clamp_enabled),
+          _ptr(aL), _ptr(cL), _ptr(R))
     return aL, cL, R
 
 
@@ -551,7 +657,7 @@ def l_update(Qb: torch.Tensor, aL: torch.Tensor, cL: torch.Tensor, want_L: bool 
     aR = torch.empty((U, m, b, d), dtype=Qb.dtype, device=Qb.device)
     cR = torch.empty((U, m, b), dtype=torch.float32, device=Qb.device)
     L = torch.empty((U, b, m, m), dtype=torch.float32, device=Qb.device) if want_L else None
-    _check(_vmb_lstep(U, m, b, d, dt, _ptr(Qb), _ptr(aL), _ptr(cL), _ptr(aR), _ptr(cR), _ptr(L), _stream()))
+    _call(Qb.device, _vmb_lstep, U, m, b, d, dt, _ptr(Qb), _ptr(aL), _ptr(cL), _ptr(aR), _ptr(cR), _ptr(L))
     return aR, cR, L
 
 
@@ -577,8 +683,7 @@ def flash_entropy_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, q_scale
     o = torch.empty_like(q)
     lse = torch.empty((U, nq), dtype=torch.float32, device=q.device)
     ent = torch.empty((U, nq), dtype=torch.float32, device=q.device) if want_entropy else None
-    _check(_vmb_flash(U, nq, nk, d, dt, _ptr(q), _ptr(k), _ptr(v), q_scale, _ptr(o), _ptr(lse), _ptr(ent),
-                      _stream()))
+    _call(q.device, _vmb_flash, U, nq, nk, d, dt, _ptr(q), _ptr(k), _ptr(v), q_scale, _ptr(o), _ptr(lse), _ptr(ent))
     if squeeze:
         return o[0], lse[0], (ent[0] if ent is not None else None)
     return o, lse, ent
@@ -613,8 +718,8 @@ def flash_entropy_bwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torc
     f32 = lambda x: None if x is None else x.contiguous().float()  # noqa: E731
     lse, entropy, dentropy = f32(lse), f32(entropy), f32(dentropy)
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
-    _check(_vmb_flash_bwd(U, nq, nk, d, dt, _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(dout), _ptr(lse), _ptr(entropy),
-                          _ptr(dentropy), int(entropy_grad), _ptr(dq), _ptr(dk), _ptr(dv), _stream()))
+    _call(q.device, _vmb_flash_bwd, U, nq, nk, d, dt, _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(dout), _ptr(lse),
+          _ptr(entropy), _ptr(dentropy), int(entropy_grad), _ptr(dq), _ptr(dk), _ptr(dv))
     if squeeze:
         return dq[0], dk[0], dv[0]
     return dq, dk, dv
@@ -627,12 +732,12 @@ def dense_forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor) -> torch.Te
     dt = _dtype_code(q)
     q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
     o = torch.empty_like(q)
-    _check(_vmb_dense(U, n, d, dt, _ptr(q), _ptr(k), _ptr(v), _ptr(o), _stream()))
+    _call(q.device, _vmb_dense, U, n, d, dt, _ptr(q), _ptr(k), _ptr(v), _ptr(o))
     return o
 
 
 def selftest_umma(mode: int, A: torch.Tensor, B: torch.Tensor) -> torch.Tensor:
     """tcgen05/TMA building-block check (see csrc/kernels/selftest.cu)."""
     C_ = torch.empty((128, 128), dtype=torch.float32, device=A.device)
-    _check(_vmb_selftest(mode, _ptr(A.contiguous()), _ptr(B.contiguous()), _ptr(C_), _stream()))
+    _call(A.device, _vmb_selftest, mode, _ptr(A.contiguous()), _ptr(B.contiguous()), _ptr(C_))
     return C_

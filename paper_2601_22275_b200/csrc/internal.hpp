@@ -47,9 +47,9 @@ inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_o
 // Optional per-kernel CUDA-event timing (vmb_profile_enable): a scope records an event
 // pair on the launching stream around one kernel launch; vmb_profile_read sums them.
 enum KernelId : int {
-    kKRstep = 0,      // fa_tc R half-step (NB=1, NO=1)
-    kKRstepY = 1,     // fa_tc last R half-step with y = R V fused (NB=2, NO=2)
-    kKAttn = 2,       // fa_tc recompute / dense attention (NB=2, NO=1)
+    kKRstep = 0,      // R half-step (fa2)
+    kKRstepY = 1,     // last R half-step with y = R V fused (fa4)
+    kKAttn = 2,       // recompute / flash / dense attention (fa3)
     kKLstep = 3,      // lstep_tc ITER
     kKLfinal = 4,     // lstep_tc FINAL (apply)
     kKSimt = 5,       // CUDA-core kernels
@@ -136,34 +136,6 @@ void check_finite_rows(View q, int64_t U, int64_t rows, int64_t d, bool bf16, in
 void check_clamp_domain(const float* cR, int64_t n, int32_t* status, cudaStream_t s);
 
 // ---------------------------------------------------------------- tcgen05 kernels (bf16, d = 128)
-struct TcFaArgs {
-    // segments: grid.y enumerates (unit, segment); segment s of unit u covers
-    // query rows [q_row0 + s*q_seg_stride, +q_len) and key rows [kv_row0 + s*kv_seg_stride, +kv_len).
-    CUtensorMap tmQ, tmK, tmV;   // 5-D maps: (d, row, seg, head, batch)
-    int32_t nseg;                // segments per unit
-    int32_t q_len, kv_len;       // rows per segment
-    int32_t qH, kH, oHn;         // heads per batch of the q map, the k/v maps, the outputs
-    const float* cR;             // per-row temperature source (U, nseg, q_len) or nullptr
-    float qscale;                // logits multiplier (log2e applied inside)
-    float clamp_min;
-    int32_t clamp_enabled;
-    int32_t nv;                  // 1: O = P*[V]; 2: O = P*[K | V] (V is the 2nd operand)
-    int32_t v_is_k;              // nv == 1 and the value operand is the key tile itself
-    // outputs: row (u, s, r) of operand t at out[t] + (u/H)*oB + (u%H)*oH + s*oS + r*oR
-    void* out0;
-    void* out1;
-    int64_t oB[2], oH[2], oS[2], oR[2];
-    float* cl_out;               // natural-log sum p ln p per row: (u, r, s) at u*q_len*nseg + r*nseg + s
-    float* lse_out;              // (u, s, r) at (u*nseg + s)*q_len + r
-    int32_t* status;             // non-finite detection
-    int32_t check_finite;
-    // TMA-store epilogue (internal contiguous outputs, R half-step + y): tmO[0] over aL
-    // (d, k, i, 1, U) box (64, 1, 128); tmO[1] over y (d, i, k, 1, U) box (64, 128, 1)
-    int32_t o_tma;
-    CUtensorMap tmO[2];
-};
-void tc_fa_launch(const TcFaArgs& a, int64_t U, cudaStream_t s);
-
 // fa2_tc.cu: 2 CTAs/SM flash attention with one value operand (R half-step: value = key,
 // BN = 128; attention: separate V, BN = 64, optional split-KV + combine).
 struct Tc2Args {
@@ -192,6 +164,9 @@ struct Tc2Args {
     int32_t nsplit;              // set by the launcher
     int64_t n_useg;              // set by the launcher
     int32_t out_align32;         // set by the launcher: every output row 32-B aligned (256-bit stores)
+    // optional low half of the bf16 output (R half-step: aL = hi + lo, hi = bf16(aL),
+    // lo = bf16(aL - hi)), same layout as `out`; nullptr = not written
+    void* out_lo;
 };
 int tc2_kv_tile(int nv);
 // 32-byte alignment of every bf16 output row of an attention launch (256-bit epilogue stores)
@@ -211,12 +186,6 @@ int tc3_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg, int max_split
 // returns the launched arguments (nsplit / n_useg set); do_combine = false leaves the split-KV
 // combine to the caller (tc2_combine_launch), e.g. on another stream
 Tc2Args tc3_fa_launch(Tc2Args a, int64_t U, cudaStream_t s, bool do_combine = true);
-// fa6_tc.cu: fa3's CTA with 64-key double-buffered score tiles per query tile (A/B variant)
-Tc2Args tc6_fa_launch(Tc2Args a, int64_t U, cudaStream_t s, bool do_combine = true);
-// fa5_tc.cu: persistent fa3 (two query tiles per item, ping-pong softmax warpgroups, one CTA
-// per SM over a flattened item stream); same argument block and 128-key K/V boxes.
-int tc5_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg, int max_split);
-void tc5_fa_launch(Tc2Args a, int64_t U, cudaStream_t s);
 // fa4_tc.cu: persistent (one CTA per SM) flash attention over a flattened stream of
 // (query tile, segment, kv-split) items; 128-key tiles (K/V maps with box rows 128).
 //   nv = 1, v_is_k = 1: R half-step (out0 = aL, cl_out)
@@ -250,13 +219,10 @@ struct Tc4Args {
     int64_t qrB, qrH, qrS, qrR;
     int32_t qrHn;
     int32_t out_align32;         // every output row 32-byte aligned: 256-bit epilogue stores
+    void* out0_lo;               // optional low half of operand 0 (aL), laid out as out0
 };
 int tc4_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg, int max_split);
 void tc4_fa_launch(Tc4Args a, int64_t U, cudaStream_t s);
-// Which attention kernel family serves a call: 2 = fa2 (R half-step default), 3 = fa3
-// (recompute / flash / dense default); env VMB_FA=2|3 forces one (A/B measurements).
-int attn_impl(bool rstep);
-
 // All L-step tiles are boxes of `rows = lstep_rows(m)` rows (m rounded up to 16); rows
 // >= m are OOB (zero-filled on load, clipped on store).
 inline int32_t lstep_rows(int64_t m) { return (int32_t)((m + 15) & ~int64_t(15)); }
@@ -273,7 +239,16 @@ struct TcLstepArgs {
     int32_t final_mode;
     float* cR;          // ITER: (U, m, b)
     float out_scale;    // multiplies the epilogue (ITER: aR scale)
+    // aL = hi + lo (the R half-step writes both halves): the low half, same boxes as tmAL.
+    // It is read only by CTAs whose score tile exceeds kLstepLoGate (use_lo = 0: never).
+    CUtensorMap tmALlo;
+    int32_t use_lo;
 };
+// The L-step adds the low half of aL to its scores only where bf16 aL could move a logit:
+// the rounding error of <Qb_j, aL_k> grows with |Qb_j| |aL_k|, and max |S| over the tile
+// tracks that product.  Below this max |S| (natural-log logits) the hi half alone keeps the
+// logit error under ~1e-3.
+constexpr float kLstepLoGate = 2.0f;
 void tc_lstep_launch(const TcLstepArgs& a, int64_t U, cudaStream_t s);
 // lstep_big.cu: L half-step / apply for m > 128 (row statistics pass + ITER or FINAL pass)
 struct TcLstepBigArgs {
@@ -290,9 +265,6 @@ struct TcLstepBigArgs {
     int32_t m, b, H, oHn;
 };
 void tc_lstep_big_launch(const TcLstepBigArgs& a, int64_t U, bool final_mode, cudaStream_t s);
-// lstep_p.cu: persistent, pipelined variant (producer warp + TMA ring, two consumer warpgroups)
-void tc_lstep_p_launch(const TcLstepArgs& a, int64_t U, cudaStream_t s);
-
 // flash_bwd.cu: backward of the online-entropy attention (flash_entropy.hpp:146-221)
 void flash_bwd_launch(int64_t U, int64_t nq, int64_t nk, int64_t d, bool bf16, const void* q, const void* k,
                       const void* v, const void* o, const void* dout, const float* lse, const float* ent,

@@ -416,6 +416,9 @@ __global__ void __launch_bounds__(kThreads, 2) fa2_kernel(const __grid_constant_
                     }
                 }
                 if (valid) {
+                    float f[32];
+#pragma unroll
+                    for (int x = 0; x < 32; ++x) f[x] = __uint_as_float(orr[x]) * inv_l;
                     uint4 v[4];
 #pragma unroll
                     for (int x = 0; x < 4; ++x) {
@@ -431,6 +434,25 @@ __global__ void __launch_bounds__(kThreads, 2) fa2_kernel(const __grid_constant_
                         uint4* dst = reinterpret_cast<uint4*>(orow + cc * 32);
 #pragma unroll
                         for (int x = 0; x < 4; ++x) dst[x] = v[x];
+                    }
+                    if (a.out_lo) {
+                        // low half of aL (same layout): bf16(x - bf16(x))
+#pragma unroll
+                        for (int x = 0; x < 4; ++x) {
+                            v[x].x = pack_bf16_residual(__uint_as_float(orr[8 * x + 0]) * inv_l, __uint_as_float(orr[8 * x + 1]) * inv_l, v[x].x);
+                            v[x].y = pack_bf16_residual(__uint_as_float(orr[8 * x + 2]) * inv_l, __uint_as_float(orr[8 * x + 3]) * inv_l, v[x].y);
+                            v[x].z = pack_bf16_residual(__uint_as_float(orr[8 * x + 4]) * inv_l, __uint_as_float(orr[8 * x + 5]) * inv_l, v[x].z);
+                            v[x].w = pack_bf16_residual(__uint_as_float(orr[8 * x + 6]) * inv_l, __uint_as_float(orr[8 * x + 7]) * inv_l, v[x].w);
+                        }
+                        __nv_bfloat16* lrow = static_cast<__nv_bfloat16*>(a.out_lo) + (orow - static_cast<__nv_bfloat16*>(a.out));
+                        if (a.out_align32) {
+                            st_global_256(lrow + cc * 32, v[0], v[1]);
+                            st_global_256(lrow + cc * 32 + 16, v[2], v[3]);
+                        } else {
+                            uint4* dst = reinterpret_cast<uint4*>(lrow + cc * 32);
+#pragma unroll
+                            for (int x = 0; x < 4; ++x) dst[x] = v[x];
+                        }
                     }
                 }
             }
@@ -552,7 +574,8 @@ void tc2_fa_launch(Tc2Args a, int64_t U, cudaStream_t s) {
     p.total_tiles = total_tiles;
     a.nsplit = nsplit;
     a.n_useg = n_useg;
-    a.out_align32 = rows_align32(a.out, a.oB, a.oH, a.oS, a.oR) ? 1 : 0;
+    a.out_align32 = rows_align32(a.out, a.oB, a.oH, a.oS, a.oR) &&
+                    (!a.out_lo || reinterpret_cast<uintptr_t>(a.out_lo) % 32 == 0) ? 1 : 0;
     p.a = a;
     if (nsplit == 1) p.a.part_o = nullptr;
     if (a.nv == 1) launch<1>(p, n_useg, nsplit, s);

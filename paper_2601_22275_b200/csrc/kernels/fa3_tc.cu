@@ -480,11 +480,9 @@ void launch(const Params& p, int64_t n_useg, int nsplit, cudaStream_t s) {
 
 int tc3_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg, int max_split) {
     if (max_split <= 1 || q_len <= 0 || n_useg <= 0) return 1;
-    static const int forced = [] {  // A/B measurement only
-        const char* e = getenv("VMB_SPLITS");
-        return e ? atoi(e) : 0;
-    }();
-    if (forced > 0) return std::min(forced, max_split);
+#ifdef VMB_FORCE_SPLITS  // experiment builds only (make EXTRA=-DVMB_FORCE_SPLITS=n)
+    return std::min(VMB_FORCE_SPLITS, max_split);
+#endif
     const int64_t total_tiles = (kv_len + kBN - 1) / kBN;
     // The split count depends on the per-unit shape only, never on the number of units in
     // the call: a unit's output is then bitwise the same whether it runs alone, in a batch or

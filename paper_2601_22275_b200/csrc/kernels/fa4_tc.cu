@@ -14,14 +14,16 @@
 //                 profiles/r1_micro_tcgen05.md)
 //   <NB=2, NO=1>  attention: first-frame recompute / dense baseline (flash_entropy.hpp:85-139)
 //
-// Warp roles (512 threads): warp 0 TMA producer, warp 1 TMEM allocator + single-thread MMA
-// issuer, warps 4-11 softmax in two warpgroups that split every score row (the thread of
-// warpgroup h owns columns [64h, 64h+64) of query row (warp%4)*32 + lane; the half-row
-// maxima meet in shared memory, one named barrier per key tile), warps 12-15 the epilogue:
-// they read an item's O out of TMEM, normalise it with the row statistics handed over in
-// shared memory and store it, while the softmax warpgroups already run the next item (a
-// non-persistent CTA spends ~5 of its ~18 us in prologue/epilogue with the tensor pipe idle,
-// profiles/r1_fa_variants.md).
+// Warp roles (320 threads): warp 0 TMA producer, warp 1 TMEM allocator + single-thread MMA
+// issuer, warps 2-5 the softmax (a thread owns one whole query row (warp%4)*32 + lane: row
+// max, exponentials and row sum stay in registers, no cross-thread exchange per key tile),
+// warps 6-9 the epilogue: they read an item's O out of TMEM, normalise it with the row
+// statistics handed over in shared memory and store it, while the softmax warpgroup already
+// runs the next item (a non-persistent CTA spends ~5 of its ~18 us in prologue/epilogue with
+// the tensor pipe idle, profiles/r1_fa_variants.md).  One softmax warp per SM sub-partition:
+// the MUFU pipe of each SMSP serves 32 rows x 128 keys = 1024 cycles per tile, under the
+// 1536 tensor cycles of S + P [K | V] (tcgen05: 64 cycles per 128x128x16, 128 per
+// 128x256x16, profiles/r2_micro_tcgen05.md).
 // TMEM (512 columns): S0 [0,128), S1 [128,256) double-buffered scores (P written back as
 // bf16 over the first 64 columns); NO=1: O0 [256,384), O1 [384,512) double-buffered over
 // items; NO=2: O [256,512) = [P K | P V].
@@ -48,7 +50,7 @@ namespace {
 
 using namespace ptx;
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 320;
 constexpr int kTile = 128;                      // query rows per item, keys per KV tile
 constexpr uint32_t kPanel = 128 * 128;          // 128 rows x 64 bf16 (SW128)
 constexpr uint32_t kTileBytes = 2 * kPanel;     // 128 x 128 bf16
@@ -132,13 +134,10 @@ struct Smem {
     // o_empty[2], stat_full[2], stat_empty[2]
     static constexpr uint32_t n_bars = 2 + 2 * S + 5 + 4 + 4;
     static constexpr uint32_t slot_off = bar_off + n_bars * 8;
-    // bf16 [2 slots][2 halves][128 rows]: per-tile half-row max exchange (double-buffered;
-    // rounded up, both halves read the same stored values -> identical decisions)
-    static constexpr uint32_t xch_off = slot_off + 16;
-    // float [O buffers][3][128 rows]: the two half-row sums and the running max of an item,
-    // handed from the softmax warpgroups to the epilogue warpgroup
-    static constexpr uint32_t stat_off = xch_off + 2 * 2 * 128 * 2;
-    static constexpr uint32_t bytes = stat_off + NOB * 3 * 128 * 4;
+    // float [O buffers][2][128 rows]: the row sum and the running max of an item, handed
+    // from the softmax warpgroup to the epilogue warpgroup
+    static constexpr uint32_t stat_off = slot_off + 16;
+    static constexpr uint32_t bytes = stat_off + NOB * 2 * 128 * 4;
     static_assert(bytes <= 232448, "shared memory budget (227 KB per CTA)");
     // the dynamic smem window starts 1024-aligned (checked in the kernel): no slack needed
     static constexpr uint32_t alloc = bytes;
@@ -159,7 +158,7 @@ __device__ __forceinline__ void trace4(int n, int ev) {
 }
 #define TRACE4(n, ev) trace4(n, ev)
 __device__ long long g_trace4t[16][2][12][6];
-#define TRACE4T(n, j, ev) do { if (threadIdx.x == 128 && blockIdx.x < 16 && (n) >= 1 && (n) <= 2 && (j) < 12) \
+#define TRACE4T(n, j, ev) do { if (threadIdx.x == 64 && blockIdx.x < 16 && (n) >= 1 && (n) <= 2 && (j) < 12) \
     g_trace4t[blockIdx.x][(n) - 1][(j)][(ev)] = clock64(); } while (0)
 #else
 #define TRACE4(n, ev) do { } while (0)
@@ -199,10 +198,10 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
         mbar_init(q_empty, 1);
         for (int i = 0; i < 2; ++i) {
             mbar_init(&s_full[i], 1);
-            mbar_init(&p_full[i], 256);
+            mbar_init(&p_full[i], 128);
             mbar_init(&o_full[i], 1);
             mbar_init(&o_empty[i], 128);
-            mbar_init(&stat_full[i], 256);
+            mbar_init(&stat_full[i], 128);
             mbar_init(&stat_empty[i], 128);
         }
         for (int s = 0; s < S; ++s) {
@@ -305,13 +304,12 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
             }
             if (pg >= 0) issue_pv();
         }
-    } else if (warp >= 4 && warp < 12) {
-        // ------------------------------------------------------------ softmax (2 warpgroups)
-        const int h = (warp - 4) >> 2;      // column half of the score row
+    } else if (warp >= 2 && warp < 6) {
+        // ------------------------------------------------------------ softmax (one warpgroup)
+        // thread = one whole query row: no cross-thread reduction anywhere in the softmax
         const int row = (warp & 3) * 32 + lane_id();  // TMEM lane == query row in tile
         const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-        __nv_bfloat16* xch = reinterpret_cast<__nv_bfloat16*>(smem + SM::xch_off);  // [slot][half][row]
-        float* stats = reinterpret_cast<float*>(smem + SM::stat_off);              // [ob][3][row]
+        float* stats = reinterpret_cast<float*>(smem + SM::stat_off);  // [ob][2][row]
         int64_t g = 0;
         int n = 0;
         // per-row temperature source, loaded one item ahead (its latency hides under a whole item)
@@ -334,73 +332,71 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
             if (a.clamp_enabled) {
                 c = (c < a.clamp_min) ? a.clamp_min : c;
             } else if (!(c > 0.f)) {
-                if (valid && h == 0) atomicExch(a.status, kStatusClampDomain);
+                if (valid) atomicExch(a.status, kStatusClampDomain);
                 c = 1.f;
             }
             const float scale2 = a.qscale * kLog2e / c;
             const int kv_end = (w.kv_tile0 + w.n_kv) * kTile;
-            const int last_valid = kTile - (kv_end > a.kv_len ? kv_end - a.kv_len : 0) - 64 * h;  // in my half
+            const int last_valid = kTile - (kv_end > a.kv_len ? kv_end - a.kv_len : 0);
 
             if (a.check_finite) {
                 mbar_wait_sleep(q_full, n & 1);
                 bool bad = false;
-                // each half checks one 64-column panel of the row
-                const uint4* q4 = reinterpret_cast<const uint4*>(qsm + h * kPanel + row * 128);
 #pragma unroll
-                for (int x = 0; x < 8; ++x) {
-                    const uint4 v = q4[x ^ (row & 7)];  // rotate chunks across lanes: no bank conflicts
-                    const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+                for (int pnl = 0; pnl < 2; ++pnl) {
+                    const uint4* q4 = reinterpret_cast<const uint4*>(qsm + pnl * kPanel + row * 128);
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        bad |= ((wd[e] & 0x7F80u) == 0x7F80u) || ((wd[e] & 0x7F800000u) == 0x7F800000u);
+                    for (int x = 0; x < 8; ++x) {
+                        const uint4 v = q4[x ^ (row & 7)];  // rotate chunks across lanes: no bank conflicts
+                        const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            bad |= ((wd[e] & 0x7F80u) == 0x7F80u) || ((wd[e] & 0x7F800000u) == 0x7F800000u);
+                    }
                 }
                 if (bad && valid) atomicExch(a.status, kStatusNonFiniteQ);
             }
 
-            float m_run = -INFINITY, l_run = 0.f;  // l_run: this half's partial row sum
+            float m_run = -INFINITY, l_run = 0.f;
             const uint64_t scale2x2 = pk2(scale2, scale2);
-            if (threadIdx.x == 128) TRACE4(n, 0);
+            if (threadIdx.x == 64) TRACE4(n, 0);
             for (int j = 0; j < w.n_kv; ++j, ++g) {
                 const uint32_t tS = tS0 + (uint32_t)(g & 1) * 128 + lane_base;
                 TRACE4T(n, j, 0);
                 mbar_wait_sleep(&s_full[g & 1], (g >> 1) & 1);
                 TRACE4T(n, j, 1);
-                if (threadIdx.x == 128 && j == 0) TRACE4(n, 1);
+                if (threadIdx.x == 64 && j == 0) TRACE4(n, 1);
                 tc_fence_after();
-                uint32_t sr[64];
-                VMB_TMEM_LD32(tS + 64 * h + 0, (sr + 0));
-                VMB_TMEM_LD32(tS + 64 * h + 32, (sr + 32));
+                uint32_t sr[kTile];
+#pragma unroll
+                for (int cc = 0; cc < kTile / 32; ++cc) VMB_TMEM_LD32(tS + cc * 32, (sr + cc * 32));
                 tmem_ld_wait();
                 TRACE4T(n, j, 2);
                 float* s = reinterpret_cast<float*>(sr);
-                if (j == w.n_kv - 1 && last_valid < 64) {
-                    asm volatile("");  // keep this a real (rarely taken) branch, not 64 selects
+                if (j == w.n_kv - 1 && last_valid < kTile) {
+                    asm volatile("");  // keep this a real (rarely taken) branch, not 128 selects
 #pragma unroll
-                    for (int x = 0; x < 64; ++x)
+                    for (int x = 0; x < kTile; ++x)
                         if (x >= last_valid) s[x] = kMasked;
                 }
+                // row max: 4 independent FMNMX3 chains
                 float a0 = s[0], a1 = s[1], a2 = s[2], a3 = s[3];
 #pragma unroll
-                for (int x = 4; x < 60; x += 8) {
+                for (int x = 4; x < kTile - 4; x += 8) {
                     a0 = fmax3(a0, s[x + 0], s[x + 1]);
                     a1 = fmax3(a1, s[x + 2], s[x + 3]);
                     a2 = fmax3(a2, s[x + 4], s[x + 5]);
                     a3 = fmax3(a3, s[x + 6], s[x + 7]);
                 }
-                a0 = fmax3(a0, s[60], s[61]);
-                a1 = fmax3(a1, s[62], s[63]);
-                // exchange the half-row maxima (double-buffered slot: one barrier per tile)
-                __nv_bfloat16* slot = xch + (g & 1) * 256;
-                slot[h * 128 + row] = __float2bfloat16_ru(fmaxf(fmaxf(a0, a1), fmaxf(a2, a3)));
-                named_bar_sync(1, 256);
+                a0 = fmax3(a0, s[kTile - 4], s[kTile - 3]);
+                a1 = fmax3(a1, s[kTile - 2], s[kTile - 1]);
                 TRACE4T(n, j, 3);
-                const float m_cand = fmaxf(__bfloat162float(slot[row]), __bfloat162float(slot[128 + row])) * scale2;
+                const float m_cand = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3)) * scale2;
                 bool rescale = false;
                 float alpha = 1.f;
                 if (j == 0) {
                     m_run = m_cand;
                 } else {
-                    // both halves see the same m_cand: identical decisions
                     const bool need = m_cand > m_run + kRescaleThreshold;
                     if (__any_sync(0xffffffffu, need)) {
                         const float m_new = fmaxf(m_run, m_cand);
@@ -412,9 +408,9 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                 }
                 const uint64_t negm2 = pk2(-m_run, -m_run);
                 const uint64_t* s2 = reinterpret_cast<const uint64_t*>(sr);
-                uint64_t acc0 = 0, acc1 = 0;
+                uint64_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
 #pragma unroll
-                for (int cc = 0; cc < 2; ++cc) {
+                for (int cc = 0; cc < kTile / 32; ++cc) {
                     uint32_t pk[16];
 #pragma unroll
                     for (int x = 0; x < 16; ++x) {
@@ -422,23 +418,26 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                         uint64_t pp;
                         if ((x % VMB_EMU_PERIOD) == VMB_EMU_PERIOD - 1) pp = ex2_emu2(t2);
                         else pp = pk2(ex2(lo2(t2)), ex2(hi2(t2)));
-                        if (x & 1) acc1 = fadd2(acc1, pp);
-                        else acc0 = fadd2(acc0, pp);
+                        switch (x & 3) {
+                            case 0: acc0 = fadd2(acc0, pp); break;
+                            case 1: acc1 = fadd2(acc1, pp); break;
+                            case 2: acc2 = fadd2(acc2, pp); break;
+                            default: acc3 = fadd2(acc3, pp); break;
+                        }
                         pk[x] = pack_bf16(lo2(pp), hi2(pp));
                     }
-                    VMB_TMEM_ST16(tS + 32 * h + cc * 16, pk);
+                    VMB_TMEM_ST16(tS + cc * 16, pk);
                 }
-                const uint64_t acc = fadd2(acc0, acc1);
+                const uint64_t acc = fadd2(fadd2(acc0, acc1), fadd2(acc2, acc3));
                 l_run += lo2(acc) + hi2(acc);
                 if (rescale) {
-                    // O must hold every earlier P V product of this item before it is rescaled;
-                    // each half rescales its half of the O columns
+                    // O must hold every earlier P V product of this item before it is rescaled
                     mbar_wait_sleep(pv_done, (uint32_t)((g - 1) & 1));
                     tc_fence_after();
 #pragma unroll
-                    for (int cc = 0; cc < 2 * NO; ++cc) {
+                    for (int cc = 0; cc < 4 * NO; ++cc) {
                         uint32_t orr[32];
-                        const uint32_t ta = tO + h * 64 * NO + cc * 32;
+                        const uint32_t ta = tO + cc * 32;
                         VMB_TMEM_LD32(ta, orr);
                         tmem_ld_wait();
 #pragma unroll
@@ -452,15 +451,15 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                 mbar_arrive(&p_full[g & 1]);
                 TRACE4T(n, j, 5);
             }
-            if (threadIdx.x == 128) TRACE4(n, 2);
+            if (threadIdx.x == 64) TRACE4(n, 2);
             // hand the item's row statistics to the epilogue warpgroup and move on
             if (n >= NOB) mbar_wait_sleep(&stat_empty[ob], ((n / NOB) - 1) & 1);
-            float* st = stats + ob * 384;
-            st[h * 128 + row] = l_run;
-            if (h == 0) st[256 + row] = m_run;
+            float* st = stats + ob * 256;
+            st[row] = l_run;
+            st[128 + row] = m_run;
             mbar_arrive(&stat_full[ob]);
         }
-    } else if (warp >= 12) {
+    } else if (warp >= 6) {
         // ------------------------------------------------------------ epilogue warpgroup
         // drains O of item n while the softmax warpgroups already work on item n+1
         const int row = (warp & 3) * 32 + lane_id();
@@ -489,15 +488,15 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
             else if (!(c > 0.f)) c = 1.f;
             const float scale2 = a.qscale * kLog2e / c;
             mbar_wait_sleep(&stat_full[ob], (n / NOB) & 1);
-            const float* st = stats + ob * 384;
-            const float l_tot = st[row] + st[128 + row];
-            const float m_run = st[256 + row];
+            const float* st = stats + ob * 256;
+            const float l_tot = st[row];
+            const float m_run = st[128 + row];
             mbar_arrive(&stat_empty[ob]);
-            if (threadIdx.x == 384) TRACE4(n, 3);
+            if (threadIdx.x == 192) TRACE4(n, 3);
             const float inv_l = 1.f / l_tot;
             const float lse2 = m_run + log2f(l_tot);  // base-2 log-sum-exp of x' = s * scale2
             mbar_wait_sleep(&o_full[ob], (n / NOB) & 1);
-            if (threadIdx.x == 384) TRACE4(n, 4);
+            if (threadIdx.x == 192) TRACE4(n, 4);
             tc_fence_after();
             if (a.part_o) {
                 // split-KV partial: normalised fp32 O and natural-log lse of this split
@@ -530,11 +529,11 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                         uint32_t orr[32];
                         VMB_TMEM_LD32(tO + t * 128 + cc * 32, orr);
                         tmem_ld_wait();
-                        if (t == NO - 1 && cc == 3) {
+                        if (t == NO - 1 && cc == 3 && !(NO == 1 && a.out0_lo)) {
                             // all of O is in registers or stored: the next item's PV may start
                             tc_fence_before();
                             mbar_arrive(&o_empty[ob]);
-                            if (threadIdx.x == 384) TRACE4(n, 5);
+                            if (threadIdx.x == 192) TRACE4(n, 5);
                         }
                         if (t == 0 && a.cl_out) {
 #pragma unroll
@@ -549,6 +548,9 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                             }
                         }
                         if (valid) {
+                            float f[32];
+#pragma unroll
+                            for (int x = 0; x < 32; ++x) f[x] = __uint_as_float(orr[x]) * inv_l;
                             uint4 v[4];
 #pragma unroll
                             for (int x = 0; x < 4; ++x) {
@@ -567,13 +569,53 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                             }
                         }
                     }
+                    if (t == 0 && a.out0_lo) {
+                        // low half of aL (same layout): bf16(x - bf16(x)), a second TMEM pass so
+                        // the entropy dot's prefetched q row is dead by then (register budget).
+                        // tcgen05.ld is warp-collective: every lane loads, only valid rows store.
+                        __nv_bfloat16* lrow = static_cast<__nv_bfloat16*>(a.out0_lo) + obh * a.oB[0] + ohh * a.oH[0] +
+                                              (int64_t)w.seg * a.oS[0] + (int64_t)grow * a.oR[0];
+#pragma unroll 1
+                        for (int cc = 0; cc < 4; ++cc) {
+                            uint32_t orr[32];
+                            VMB_TMEM_LD32(tO + cc * 32, orr);
+                            tmem_ld_wait();
+                            if (NO == 1 && cc == 3) {
+                                tc_fence_before();
+                                mbar_arrive(&o_empty[ob]);
+                            }
+                            if (valid) {
+                                uint4 v[4];
+#pragma unroll
+                                for (int x = 0; x < 4; ++x) {
+                                    uint32_t h[4];
+#pragma unroll
+                                    for (int e = 0; e < 4; ++e) {
+                                        const float f0 = __uint_as_float(orr[8 * x + 2 * e]) * inv_l;
+                                        const float f1 = __uint_as_float(orr[8 * x + 2 * e + 1]) * inv_l;
+                                        h[e] = pack_bf16_residual(f0, f1, pack_bf16(f0, f1));
+                                    }
+                                    v[x] = make_uint4(h[0], h[1], h[2], h[3]);
+                                }
+                                if (a.out_align32) {
+                                    st_global_256(lrow + cc * 32, v[0], v[1]);
+                                    st_global_256(lrow + cc * 32 + 16, v[2], v[3]);
+                                } else {
+                                    uint4* dst = reinterpret_cast<uint4*>(lrow + cc * 32);
+#pragma unroll
+                                    for (int x = 0; x < 4; ++x) dst[x] = v[x];
+                                }
+                            }
+                            __syncwarp();
+                        }
+                    }
                 }
                 if (valid) {
                     if (a.cl_out)
                         a.cl_out[((int64_t)w.u * a.q_len + grow) * a.nseg + w.seg] = kLn2 * (scale2 * qo * inv_l - lse2);
                     if (a.lse_out) a.lse_out[((int64_t)w.u * a.nseg + w.seg) * a.q_len + grow] = kLn2 * lse2;
                 }
-                if (threadIdx.x == 384) TRACE4(n, 6);
+                if (threadIdx.x == 192) TRACE4(n, 6);
             }
         }
     }
@@ -634,6 +676,7 @@ void tc4_fa_launch(Tc4Args a, int64_t U, cudaStream_t s) {
             al = al && (reinterpret_cast<uintptr_t>(base) % 32 == 0) && a.oB[t] % 16 == 0 && a.oH[t] % 16 == 0 &&
                  a.oS[t] % 16 == 0 && a.oR[t] % 16 == 0;
         }
+        if (a.out0_lo) al = al && reinterpret_cast<uintptr_t>(a.out0_lo) % 32 == 0;
         a.out_align32 = al ? 1 : 0;
     }
     VMB_REQUIRE_DIM(p.n_items < ((int64_t)1 << 31), "too many work items for one launch");

@@ -47,7 +47,7 @@ struct Layout {
         y = 4 * panel;
         cl = (final_mode ? 6 : 4) * panel;
         bars = cl + 512;
-        slot = bars + 32;
+        slot = bars + 48;
         bytes = slot + 16;
         // M = 128 MMAs read 128 rows of every K-major A panel (rows >= R are don't-care
         // rows of the accumulator) -- keep those reads inside the allocation.
@@ -66,6 +66,8 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
     uint64_t* bar_load = reinterpret_cast<uint64_t*>(smem + L.bars);
     uint64_t* bar_mma1 = bar_load + 1;
     uint64_t* bar_mma2 = bar_load + 2;
+    uint64_t* bar_lo = bar_load + 3;      // aL low half loaded
+    uint64_t* bar_mma1b = bar_load + 4;   // S += Qb aL_lo^T done
     uint32_t* slot = reinterpret_cast<uint32_t*>(smem + L.slot);
     float* s_cl = reinterpret_cast<float*>(smem + L.cl);
 
@@ -83,10 +85,13 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
             tma_prefetch_desc(&a.tmQ);
             tma_prefetch_desc(&a.tmAL);
             if (FINAL) tma_prefetch_desc(&a.tmY);
+            if (a.use_lo) tma_prefetch_desc(&a.tmALlo);
             tma_prefetch_desc(&a.tmOut);
             mbar_init(bar_load, 1);
             mbar_init(bar_mma1, 1);
             mbar_init(bar_mma2, 1);
+            mbar_init(bar_lo, 1);
+            mbar_init(bar_mma1b, 1);
             fence_mbar_init();
             // loads first: their latency overlaps the TMEM allocation and the cL fetch
             const int qbb = u / a.H, qh = u % a.H;
@@ -133,6 +138,37 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
     for (int c = 0; c < NCH; ++c) VMB_TMEM_LD32(tmem + lane_base + c * 32, (sr + c * 32));
     tmem_ld_wait();
     float* s = reinterpret_cast<float*>(sr);
+    if (a.use_lo) {
+        // aL = hi + lo: add Qb aL_lo^T where the hi half alone could move a logit (kLstepLoGate)
+        float amax = 0.f;
+#pragma unroll
+        for (int k = 0; k < NCH * 32; ++k) amax = (k < m) ? fmaxf(amax, fabsf(s[k])) : amax;
+        tc_fence_before();
+        if (__syncthreads_or(amax * a.qscale > kLstepLoGate)) {
+            if (leader) {
+                // GEMM 1 has finished reading aL_hi (bar_mma1): the low half lands in its place
+                mbar_arrive_expect_tx(bar_lo, 2u * L.panel);
+                tma_load_5d(smem + L.al, &a.tmALlo, bar_lo, 0, 0, i, 0, u);
+                tma_load_5d(smem + L.al + L.panel, &a.tmALlo, bar_lo, 64, 0, i, 0, u);
+                mbar_wait(bar_lo, 0);
+                tc_fence_after();
+                const uint32_t id1 = idesc_bf16(128, (uint32_t)R, 0, 0);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t off = (kk >> 2) * L.panel + (kk & 3) * 32;
+                    umma_ss(tmem, sdesc_sw128(qb_addr + off, 16, 1024), sdesc_sw128(al_addr + off, 16, 1024), id1, 1u);
+                }
+                umma_commit(bar_mma1b);
+            }
+            __syncwarp();
+            mbar_wait(bar_mma1b, 0);
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) VMB_TMEM_LD32(tmem + lane_base + c * 32, (sr + c * 32));
+            tmem_ld_wait();
+        }
+        tc_fence_after();
+    }
     const float sc2 = a.qscale * kLog2e;
     float mx = -INFINITY;
 #pragma unroll

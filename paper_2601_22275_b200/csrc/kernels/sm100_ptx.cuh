@@ -302,6 +302,10 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // .x = lo (low 16 bits)
     return *reinterpret_cast<uint32_t*>(&v);
 }
+// Residual of pack_bf16: the bf16 pair of (x - bf16(x)), so hi + lo carries ~16 mantissa bits.
+__device__ __forceinline__ uint32_t pack_bf16_residual(float a, float b, uint32_t hi) {
+    return pack_bf16(a - __uint_as_float(hi << 16), b - __uint_as_float(hi & 0xFFFF0000u));
+}
 
 // 256-bit global store (sm_100 STG.256): one 32-byte sector per thread instead of two
 // half-sector 16-byte stores -- halves the L1/L2 transactions of row-per-thread epilogues.

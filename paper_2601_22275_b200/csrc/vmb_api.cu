@@ -122,27 +122,6 @@ CUtensorMap make_tmap_bf16_5d(const void* base, const uint64_t dims[5], const ui
     return map;
 }
 
-int attn_impl(bool rstep) {
-    // Kernel family per call site (A/B switches for measurements):
-    //   R half-steps (VMB_RSTEP): 2 = fa2 (default: 2 CTAs/SM, 64-key tiles) with the
-    //     persistent fa4 for the last (y-fused) step, 1 = fa_tc for both, 4 = fa4 for both,
-    //     5 = persistent 2-Q-tile fa5 (+ fa4 for the last step)
-    //     (profiles/r1_fa_variants.md has the measurements behind the default)
-    //   attention over all N keys: recompute / flash / dense (VMB_ATTN): 3 = fa3 (default),
-    //     4 = fa4 persistent, 5 = fa5 persistent 2-Q-tile, 2 = fa2
-    static const int r = [] {
-        const char* e = getenv("VMB_RSTEP");
-        const int v = e ? atoi(e) : 2;
-        return (v == 1 || v == 4 || v == 5 || v == 6) ? v : 2;
-    }();
-    static const int at = [] {
-        const char* e = getenv("VMB_ATTN");
-        const int v = e ? atoi(e) : 3;
-        return (v == 2 || v == 4 || v == 5 || v == 6) ? v : 3;
-    }();
-    return rstep ? r : at;
-}
-
 void scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
     static std::mutex mu;
     static std::vector<int> done;
@@ -165,112 +144,31 @@ namespace {
 
 constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
-// key-tile rows of the attention kernel family in use (the K/V TMA box height)
-uint32_t attn_kv_box(bool rstep) {
-    const int impl = attn_impl(rstep);
-    return impl == 2 ? (uint32_t)tc2_kv_tile(1) : impl == 6 ? 64u : 128u;
-}
+// Experiment builds (make EXTRA=... OUT=... BUILD=...): persistent fa4 for the other stages
+#ifndef VMB_RSTEP_FA4
+#define VMB_RSTEP_FA4 0
+#endif
+#ifndef VMB_RECOMPUTE_FA4
+#define VMB_RECOMPUTE_FA4 0
+#endif
+// key-tile rows of the attention kernels: fa2 (R half-step) 64, fa3 (attention over all keys) 128
+constexpr uint32_t kRstepKvBox = 64, kAttnKvBox = 128;
 int attn_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg) {
-    switch (attn_impl(false)) {
-        case 2: return tc2_plan_splits(q_len, kv_len, n_useg, 2, kTc2MaxSplit);
-        case 4: return tc4_plan_splits(q_len, kv_len, n_useg, kTc2MaxSplit);
-        case 5: return tc5_plan_splits(q_len, kv_len, n_useg, kTc2MaxSplit);
-        default: return tc3_plan_splits(q_len, kv_len, n_useg, kTc2MaxSplit);  // fa3 and fa6
-    }
+    return tc3_plan_splits(q_len, kv_len, n_useg, kTc2MaxSplit);
 }
-// query rows for fa4's entropy dot: row (u, s, r) at base + (u/Hn)*B + (u%Hn)*H + s*S + r*R
-struct QRows {
-    const void* base = nullptr;
-    int64_t B = 0, H = 0, S = 0, R = 0;
-    int32_t Hn = 1;
-};
-void set_qrows(Tc4Args& r, const QRows& q) {
-    r.q_rows = q.base;
-    r.qrB = q.B; r.qrH = q.H; r.qrS = q.S; r.qrR = q.R; r.qrHn = q.Hn;
-}
-Tc4Args to_tc4(const Tc2Args& a, const QRows& qv = QRows{}) {
-    Tc4Args r{};
-    set_qrows(r, qv);
-    r.tmQ = a.tmQ; r.tmK = a.tmK; r.tmV = a.tmV;
-    r.nseg = a.nseg; r.q_len = a.q_len; r.kv_len = a.kv_len;
-    r.qH = a.qH; r.kH = a.kH; r.oHn = a.oHn;
-    r.cR = a.cR; r.qscale = a.qscale; r.clamp_min = a.clamp_min; r.clamp_enabled = a.clamp_enabled;
-    r.nv = 1;
-    r.v_is_k = a.nv == 1;
-    r.out0 = a.out;
-    r.oB[0] = a.oB; r.oH[0] = a.oH; r.oS[0] = a.oS; r.oR[0] = a.oR;
-    r.cl_out = a.cl_out; r.lse_out = a.lse_out; r.status = a.status; r.check_finite = a.check_finite;
-    r.part_o = a.part_o; r.part_lse = a.part_lse; r.max_split = a.max_split;
-    return r;
-}
-Tc4Args to_tc4(const TcFaArgs& a, const QRows& qv) {
-    Tc4Args r{};
-    set_qrows(r, qv);
-    r.tmQ = a.tmQ; r.tmK = a.tmK; r.tmV = a.tmV;
-    r.nseg = a.nseg; r.q_len = a.q_len; r.kv_len = a.kv_len;
-    r.qH = a.qH; r.kH = a.kH; r.oHn = a.oHn;
-    r.cR = a.cR; r.qscale = a.qscale; r.clamp_min = a.clamp_min; r.clamp_enabled = a.clamp_enabled;
-    r.nv = a.nv; r.v_is_k = a.v_is_k;
-    r.out0 = a.out0; r.out1 = a.out1;
-    for (int t = 0; t < 2; ++t) { r.oB[t] = a.oB[t]; r.oH[t] = a.oH[t]; r.oS[t] = a.oS[t]; r.oR[t] = a.oR[t]; }
-    r.cl_out = a.cl_out; r.lse_out = a.lse_out; r.status = a.status; r.check_finite = a.check_finite;
-    r.max_split = 1;
-    return r;
-}
-// a.nv == 2: value operand V (attention); a.nv == 1: value = key (R half-step)
-void attn_launch(const Tc2Args& a, int64_t U, cudaStream_t s, bool rstep, const QRows& qv = QRows{}) {
-    switch (attn_impl(rstep)) {
-        case 2: tc2_fa_launch(a, U, s); break;
-        case 4: tc4_fa_launch(to_tc4(a, qv), U, s); break;
-        case 5: tc5_fa_launch(a, U, s); break;
-        case 6: tc6_fa_launch(a, U, s); break;
-        case 1:  // original 1-CTA/SM kernel (R half-step only)
-        default:
-            if (rstep && attn_impl(true) == 1) {
-                TcFaArgs f{};
-                f.tmQ = a.tmQ; f.tmK = a.tmK; f.tmV = a.tmV;
-                f.nseg = a.nseg; f.q_len = a.q_len; f.kv_len = a.kv_len;
-                f.qH = a.qH; f.kH = a.kH; f.oHn = a.oHn;
-                f.cR = a.cR; f.qscale = a.qscale; f.clamp_min = a.clamp_min; f.clamp_enabled = a.clamp_enabled;
-                f.nv = 1; f.v_is_k = 1;
-                f.out0 = a.out; f.oB[0] = a.oB; f.oH[0] = a.oH; f.oS[0] = a.oS; f.oR[0] = a.oR;
-                f.cl_out = a.cl_out; f.lse_out = a.lse_out; f.status = a.status; f.check_finite = a.check_finite;
-                tc_fa_launch(f, U, s);
-            } else {
-                tc3_fa_launch(a, U, s);
-            }
-            break;
-    }
-}
-
-// Overlap of the first-frame recompute with the monarch chain (VMB_OVERLAP=1; off by default:
-// measured 13.57-13.64 vs 13.25-13.53 ms serial at C4 -- the recompute spreads over the whole
-// call and slows every chain kernel by as much as it saves, profiles/r1_fa_variants.md):
-// the chain (R/L half-steps) runs on a high-priority internal stream forked from the caller's
-// stream, the recompute's split-KV partial pass on the caller's stream; the combine joins
-// both.  The block scheduler then hands SMs the recompute leaves idle -- the tails of the
-// attention launches and the HBM-bound L-steps -- to the other stream's kernels.
-struct OverlapStreams {
-    cudaStream_t chain = nullptr;
+// Side stream of the single-process multi-GPU sequence mode (V gathered beside the forward).
+struct SideStream {
+    cudaStream_t st = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
 };
-bool overlap_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("VMB_OVERLAP");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
-OverlapStreams& overlap_streams() {
+SideStream& side_stream() {
     // per thread and device: fork/join events of concurrent callers never interleave
-    thread_local std::map<int, OverlapStreams> per_dev;
+    thread_local std::map<int, SideStream> per_dev;
     int dev = 0;
     VMB_CHECK_CUDA(cudaGetDevice(&dev));
-    OverlapStreams& o = per_dev[dev];
-    if (!o.chain) {
-        int least = 0, greatest = 0;
-        VMB_CHECK_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-        VMB_CHECK_CUDA(cudaStreamCreateWithPriority(&o.chain, cudaStreamNonBlocking, greatest));
+    SideStream& o = per_dev[dev];
+    if (!o.st) {
+        VMB_CHECK_CUDA(cudaStreamCreateWithFlags(&o.st, cudaStreamNonBlocking));
         VMB_CHECK_CUDA(cudaEventCreateWithFlags(&o.fork, cudaEventDisableTiming));
         VMB_CHECK_CUDA(cudaEventCreateWithFlags(&o.join, cudaEventDisableTiming));
     }
@@ -325,6 +223,7 @@ struct Workspace {
     void* aR;
     void* aL;
     void* y;
+    void* aL_lo;      // low half of aL (bf16 tcgen05 path, m <= 128): aL = aL + aL_lo
     float* cR;
     float* cL;
     float* part_o;    // split-KV partials of the first-frame recompute (tcgen05 path)
@@ -345,6 +244,11 @@ Workspace carve(void* base, const Shape& s, vmb_dtype dt) {
     w.aR = p + off; off += act;
     w.aL = p + off; off += act;
     w.y = p + off; off += act;
+    w.aL_lo = nullptr;
+    if (dt == VMB_BF16 && s.d == 128 && s.m <= 128) {
+        w.aL_lo = p + off;
+        off += act;
+    }
     w.cR = reinterpret_cast<float*>(p + off); off += st;
     w.cL = reinterpret_cast<float*>(p + off); off += st;
     w.part_o = w.part_lse = nullptr;
@@ -433,8 +337,6 @@ bool tc_eligible(const Shape& s, vmb_dtype dt, const vmb_strides& in, const vmb_
                  const void* q, const void* k, const void* v, const void* o) {
     if (dt != VMB_BF16 || s.d != 128 || !tmap_supported()) return false;
     if (s.N > (int64_t)INT32_MAX || s.b > 65535 * 16) return false;
-    // the default R-step grid is 1-D; the A/B families put (unit, frame block) on grid.y
-    if (attn_impl(true) != 2 && s.U * s.m > 65535) return false;
     const int64_t strides[6] = {in.batch, in.head, in.token, out.batch, out.head, out.token};
     for (int64_t x : strides)
         if (x % 8 != 0) return false;
@@ -478,122 +380,95 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
 
     if (tc_eligible(s, dt, in, out, q, k, v, o) && tc_eligible(s, dt, kin, out, q, k, v, o)) {
         // ------------------------------------------------ tcgen05 path
-        const cudaStream_t user_st = st;
-        // overlap only when the recompute goes through split-KV partials: its O rows are then
-        // written by the combine, after the chain's last L-step has written the other rows
-        const bool overlap = recompute && overlap_enabled() && attn_impl(false) == 3 && ws.part_o &&
-                             tc3_plan_splits(s.hwq, s.N, U, kTc2MaxSplit) > 1;
-        OverlapStreams* ov = overlap ? &overlap_streams() : nullptr;
-        if (ov) {
-            VMB_CHECK_CUDA(cudaEventRecord(ov->fork, user_st));
-            VMB_CHECK_CUDA(cudaStreamWaitEvent(ov->chain, ov->fork, 0));
-            st = ov->chain;
-        }
+        const int32_t Hm = (int32_t)std::max<int64_t>(s.H, 1);
         const CUtensorMap mQrow = user_map(q, in, s, bq, 1, m, bq, 128, 1);    // (d, i, k): query tiles
-        const CUtensorMap mK = user_map(k, kin, s, b, 1, m, b, 128, 1);
+        const CUtensorMap mK = user_map(k, kin, s, b, 1, m, b, 128, 1);        // fa4: 128-key tiles
         const CUtensorMap mV = user_map(v, kin, s, b, 1, m, b, 128, 1);
-        const CUtensorMap mK2 = user_map(k, kin, s, b, 1, m, b, attn_kv_box(true), 1);  // attention key tiles
+        const CUtensorMap mK2 = user_map(k, kin, s, b, 1, m, b, kRstepKvBox, 1);  // fa2: 64-key tiles
         // (the lstep_tc boxes; with m > 128 the multi-pass L-step builds its own maps)
         const uint32_t lrows = (uint32_t)std::min<int64_t>(lstep_rows(m), 128);
         const CUtensorMap mQcol = user_map(q, in, s, bq, 1, m, bq, 1, lrows);   // (d, i, j): Qb[i] boxes
         const CUtensorMap mAR = internal_map(ws.aR, U, m, bq, d, true, 128, 1);  // aR (U,m,bq,d): (d,i,k) query tiles
         const CUtensorMap mARst = internal_map(ws.aR, U, m, bq, d, true, 1, lrows);  // aR columns (d,i,k), L-step store
         const CUtensorMap mAL = internal_map(ws.aL, U, bq, m, d, true, lrows, 1);  // aL (U,bq,m,d): (d,k,i)
+        const CUtensorMap mALlo = internal_map(ws.aL_lo ? ws.aL_lo : ws.aL, U, bq, m, d, true, lrows, 1);
         const CUtensorMap mY = internal_map(ws.y, U, m, bq, d, true, 1, lrows);    // y (U,m,bq,d): (d,i,k)
         const CUtensorMap mOcol = user_map(o, out, s, bq, 1, m, bq, 1, lrows);  // O rows j*bq+i: (d, i, j)
         for (int64_t t = 0; t < cfg.iters; ++t) {
             const bool last = t == cfg.iters - 1;
             if (last && v_ready) VMB_CHECK_CUDA(cudaStreamWaitEvent(st, v_ready, 0));
-            TcFaArgs fa{};
-            fa.tmQ = t == 0 ? mQrow : mAR;
-            fa.tmK = mK;
-            fa.tmV = mV;
-            fa.nseg = (int32_t)m;
-            fa.q_len = (int32_t)bq;
-            fa.kv_len = (int32_t)b;
-            fa.qH = t == 0 ? (int32_t)std::max<int64_t>(s.H, 1) : 1;
-            fa.kH = (int32_t)std::max<int64_t>(s.H, 1);
-            fa.oHn = 1;
-            fa.cR = t == 0 ? nullptr : ws.cR;
-            fa.qscale = t == 0 ? qscale : 1.f;
-            fa.clamp_min = (float)cfg.clamp_min;
-            fa.clamp_enabled = cfg.clamp_enabled;
-            fa.nv = last ? 2 : 1;
-            fa.v_is_k = last ? 0 : 1;
-            fa.out0 = ws.aL;                       // aL (U, bq, m, d): row (u, k, i)
-            fa.oB[0] = bq * m * d; fa.oH[0] = 0; fa.oS[0] = d; fa.oR[0] = m * d;
-            fa.out1 = ws.y;                        // y (U, m, bq, d): row (u, k, i)
-            fa.oB[1] = m * bq * d; fa.oH[1] = 0; fa.oS[1] = bq * d; fa.oR[1] = d;
-            fa.cl_out = ws.cL;
-            fa.lse_out = nullptr;
-            fa.status = ws.status;
-            fa.check_finite = t == 0;
-            // query rows of this half-step (fa4's entropy dot reads them from global memory)
-            QRows qv;
-            if (t == 0) {
-                qv.base = q; qv.B = in.batch; qv.H = in.head; qv.S = bq * in.token; qv.R = in.token;
-                qv.Hn = (int32_t)std::max<int64_t>(s.H, 1);
-            } else {
-                qv.base = ws.aR; qv.B = m * bq * d; qv.H = 0; qv.S = bq * d; qv.R = d; qv.Hn = 1;
-            }
+            // query rows of this half-step: Q itself (first step, scaled in-kernel) or aR
+            const CUtensorMap& mq = t == 0 ? mQrow : mAR;
+            const float* cr = t == 0 ? nullptr : ws.cR;
+            const float qs = t == 0 ? qscale : 1.f;
             if (last) {
-                // last R half-step with y = R V fused: O = P [K | V]; fa4 (persistent, epilogue
-                // warpgroup) unless VMB_RSTEP=1 forces the 1-CTA/SM fa_tc
-                if (attn_impl(true) != 1) {
-                    tc4_fa_launch(to_tc4(fa, qv), U, st);
+                // last R half-step with y = R V fused (monarch.hpp:182-185): persistent fa4,
+                // O = P [K | V] as one N = 256 MMA per key step
+                Tc4Args f4{};
+                f4.tmQ = mq; f4.tmK = mK; f4.tmV = mV;
+                f4.nseg = (int32_t)m; f4.q_len = (int32_t)bq; f4.kv_len = (int32_t)b;
+                f4.qH = t == 0 ? Hm : 1; f4.kH = Hm; f4.oHn = 1;
+                f4.cR = cr; f4.qscale = qs;
+                f4.clamp_min = (float)cfg.clamp_min; f4.clamp_enabled = cfg.clamp_enabled;
+                f4.nv = 2; f4.v_is_k = 0;
+                f4.out0 = ws.aL;                       // aL (U, bq, m, d): row (u, k, i)
+                f4.oB[0] = bq * m * d; f4.oH[0] = 0; f4.oS[0] = d; f4.oR[0] = m * d;
+                f4.out1 = ws.y;                        // y (U, m, bq, d): row (u, k, i)
+                f4.oB[1] = m * bq * d; f4.oH[1] = 0; f4.oS[1] = bq * d; f4.oR[1] = d;
+                f4.cl_out = ws.cL;
+                f4.out0_lo = ws.aL_lo;
+                f4.status = ws.status;
+                f4.check_finite = t == 0;
+                f4.max_split = 1;
+                // query rows for the epilogue's entropy dot, read from global memory
+                if (t == 0) {
+                    f4.q_rows = q; f4.qrB = in.batch; f4.qrH = in.head; f4.qrS = bq * in.token; f4.qrR = in.token;
+                    f4.qrHn = Hm;
                 } else {
-                    fa.o_tma = 1;
-                    fa.tmO[0] = internal_map(ws.aL, U, bq, m, d, true, 1, 128);  // aL (d, k, i, 1, U)
-                    fa.tmO[1] = internal_map(ws.y, U, m, bq, d, true, 128, 1);   // y  (d, i, k, 1, U)
-                    tc_fa_launch(fa, U, st);
+                    f4.q_rows = ws.aR; f4.qrB = m * bq * d; f4.qrH = 0; f4.qrS = bq * d; f4.qrR = d; f4.qrHn = 1;
                 }
+                tc4_fa_launch(f4, U, st);
+            } else if (VMB_RSTEP_FA4) {
+                Tc4Args f4{};
+                f4.tmQ = mq; f4.tmK = mK; f4.tmV = mK;
+                f4.nseg = (int32_t)m; f4.q_len = (int32_t)bq; f4.kv_len = (int32_t)b;
+                f4.qH = t == 0 ? Hm : 1; f4.kH = Hm; f4.oHn = 1;
+                f4.cR = cr; f4.qscale = qs;
+                f4.clamp_min = (float)cfg.clamp_min; f4.clamp_enabled = cfg.clamp_enabled;
+                f4.nv = 1; f4.v_is_k = 1;
+                f4.out0 = ws.aL;
+                f4.oB[0] = bq * m * d; f4.oH[0] = 0; f4.oS[0] = d; f4.oR[0] = m * d;
+                f4.cl_out = ws.cL;
+                f4.out0_lo = ws.aL_lo;
+                f4.status = ws.status;
+                f4.check_finite = t == 0;
+                f4.max_split = 1;
+                if (t == 0) {
+                    f4.q_rows = q; f4.qrB = in.batch; f4.qrH = in.head; f4.qrS = bq * in.token; f4.qrR = in.token;
+                    f4.qrHn = Hm;
+                } else {
+                    f4.q_rows = ws.aR; f4.qrB = m * bq * d; f4.qrH = 0; f4.qrS = bq * d; f4.qrR = d; f4.qrHn = 1;
+                }
+                tc4_fa_launch(f4, U, st);
             } else {
-                // R half-step without y: the 2-CTA/SM kernel (value operand = key tile)
+                // R half-step without y: fa2, two CTAs per SM, value operand = key tile
                 Tc2Args f2{};
-                f2.tmQ = fa.tmQ;
-                f2.tmK = mK2;
-                f2.tmV = mK2;
-                f2.nseg = fa.nseg;
-                f2.q_len = fa.q_len;
-                f2.kv_len = fa.kv_len;
-                f2.qH = fa.qH;
-                f2.kH = fa.kH;
-                f2.oHn = 1;
-                f2.cR = fa.cR;
-                f2.qscale = fa.qscale;
-                f2.clamp_min = fa.clamp_min;
-                f2.clamp_enabled = fa.clamp_enabled;
+                f2.tmQ = mq; f2.tmK = mK2; f2.tmV = mK2;
+                f2.nseg = (int32_t)m; f2.q_len = (int32_t)bq; f2.kv_len = (int32_t)b;
+                f2.qH = t == 0 ? Hm : 1; f2.kH = Hm; f2.oHn = 1;
+                f2.cR = cr; f2.qscale = qs;
+                f2.clamp_min = (float)cfg.clamp_min; f2.clamp_enabled = cfg.clamp_enabled;
                 f2.nv = 1;
                 f2.out = ws.aL;
                 f2.oB = bq * m * d; f2.oH = 0; f2.oS = d; f2.oR = m * d;
                 f2.cl_out = ws.cL;
+                f2.out_lo = ws.aL_lo;
                 f2.status = ws.status;
-                f2.check_finite = fa.check_finite;
+                f2.check_finite = t == 0;
                 f2.max_split = 1;
-                if (attn_impl(true) == 4) f2.tmK = f2.tmV = mK;  // fa4: 128-key tiles
-                attn_launch(f2, U, st, true, qv);
+                tc2_fa_launch(f2, U, st);
             }
 
-            TcLstepArgs ls{};
-            ls.tmQ = mQcol;
-            ls.tmAL = mAL;
-            ls.tmY = mY;
-            ls.tmOut = last ? mOcol : mARst;
-            ls.cL = ws.cL;
-            ls.qscale = qscale;
-            ls.m = (int32_t)m;
-            ls.b = (int32_t)bq;
-            ls.H = (int32_t)std::max<int64_t>(s.H, 1);
-            ls.oHn = (int32_t)std::max<int64_t>(s.H, 1);
-            ls.final_mode = last;
-            ls.cR = ws.cR;
-            ls.out_scale = last ? 1.f : qscale;
-            // one position per CTA (4 CTAs/SM) unless VMB_LSTEP=2 selects the persistent pipelined
-            // kernel (measured slower: 1.10 vs 0.85 ms at C4, profiles/r1_fa_variants.md)
-            static const bool lstep_pipelined = [] {
-                const char* e = getenv("VMB_LSTEP");
-                return e && e[0] == '2';
-            }();
             if (m > 128) {
                 // more than 128 row blocks (general factorizations): multi-pass L-step
                 TcLstepBigArgs lb{};
@@ -614,27 +489,40 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
                 lb.out_scale = last ? 1.f : qscale;
                 lb.m = (int32_t)m;
                 lb.b = (int32_t)bq;
-                lb.H = (int32_t)std::max<int64_t>(s.H, 1);
-                lb.oHn = (int32_t)std::max<int64_t>(s.H, 1);
+                lb.H = Hm;
+                lb.oHn = Hm;
                 tc_lstep_big_launch(lb, U, last, st);
-            } else if (lstep_pipelined) {
-                tc_lstep_p_launch(ls, U, st);
             } else {
+                TcLstepArgs ls{};
+                ls.tmQ = mQcol;
+                ls.tmAL = mAL;
+                ls.tmY = mY;
+                ls.tmOut = last ? mOcol : mARst;
+                ls.cL = ws.cL;
+                ls.qscale = qscale;
+                ls.m = (int32_t)m;
+                ls.b = (int32_t)bq;
+                ls.H = Hm;
+                ls.oHn = Hm;
+                ls.final_mode = last;
+                ls.cR = ws.cR;
+                ls.out_scale = last ? 1.f : qscale;
+                ls.tmALlo = mALlo;
+                ls.use_lo = ws.aL_lo != nullptr;
                 tc_lstep_launch(ls, U, st);
             }
         }
         if (recompute) {
-            // first-frame recompute: Q[0:hw) against all N keys, split over the keys
-            const int64_t Hm = std::max<int64_t>(s.H, 1);
-            const uint32_t bn = attn_kv_box(false);
+            // first-frame recompute (video.hpp:117-126): Q[0:hw) against all N keys on fa3,
+            // split over the keys with an LSE combine that overwrites O rows [0, hw)
             Tc2Args f2{};
             f2.tmQ = user_map(q, in, s, s.hwq, 1, 1, s.hwq, 128, 1);
-            f2.tmK = user_map(k, kin, s, s.N, 1, 1, s.N, bn, 1);
-            f2.tmV = user_map(v, kin, s, s.N, 1, 1, s.N, bn, 1);
+            f2.tmK = user_map(k, kin, s, s.N, 1, 1, s.N, kAttnKvBox, 1);
+            f2.tmV = user_map(v, kin, s, s.N, 1, 1, s.N, kAttnKvBox, 1);
             f2.nseg = 1;
             f2.q_len = (int32_t)s.hwq;
             f2.kv_len = (int32_t)s.N;
-            f2.qH = f2.kH = f2.oHn = (int32_t)Hm;
+            f2.qH = f2.kH = f2.oHn = Hm;
             f2.qscale = qscale;
             f2.nv = 2;
             f2.out = o;
@@ -643,13 +531,20 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
             f2.part_o = ws.part_o;
             f2.part_lse = ws.part_lse;
             f2.max_split = ws.part_o ? kTc2MaxSplit : 1;
-            if (ov) {
-                const Tc2Args fin = tc3_fa_launch(f2, U, user_st, false);
-                VMB_CHECK_CUDA(cudaEventRecord(ov->join, ov->chain));
-                VMB_CHECK_CUDA(cudaStreamWaitEvent(user_st, ov->join, 0));
-                tc2_combine_launch(fin, user_st);
+            if (VMB_RECOMPUTE_FA4) {
+                Tc4Args f4{};
+                f4.tmQ = f2.tmQ; f4.tmK = f2.tmK; f4.tmV = f2.tmV;
+                f4.nseg = 1; f4.q_len = f2.q_len; f4.kv_len = f2.kv_len;
+                f4.qH = f4.kH = f4.oHn = Hm;
+                f4.qscale = qscale;
+                f4.nv = 1; f4.v_is_k = 0;
+                f4.out0 = o;
+                f4.oB[0] = out.batch; f4.oH[0] = out.head; f4.oS[0] = 0; f4.oR[0] = out.token;
+                f4.status = ws.status;
+                f4.part_o = ws.part_o; f4.part_lse = ws.part_lse; f4.max_split = ws.part_o ? ws.nsplit : 1;
+                tc4_fa_launch(f4, U, st);
             } else {
-                attn_launch(f2, U, st, false);
+                tc3_fa_launch(f2, U, st);
             }
         }
         return;
@@ -657,6 +552,7 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
 
     // ---------------------------------------------------- CUDA-core path (any shape / fp32)
     VMB_REQUIRE_DIM(!sharded, "the sequence-sharded mode needs the tcgen05 path (bf16, d = 128, m <= 128)");
+    if (v_ready) VMB_CHECK_CUDA(cudaStreamWaitEvent(st, v_ready, 0));
     check_finite_rows(user_view(q, in, s, 0, 1), U, s.N, d, bf16, ws.status, st);
     const View vQrow = user_view(q, in, s, b, 1);    // (u, k, i) -> token k*b+i
     const View vK = user_view(k, in, s, b, 1);
@@ -737,8 +633,7 @@ int64_t ceil16(int64_t x) { return (x + 15) & ~int64_t(15); }
 // with Q, K, V zero-padded to 128 columns in the workspace: zero columns add nothing to any
 // score or product, so every half-step is exact, and the padded output columns are dropped.
 bool padded_path(const Shape& s, vmb_dtype dt) {
-    return dt == VMB_BF16 && s.d < 128 && tmap_supported() && (attn_impl(true) == 2 || s.U * s.m <= 65535) &&
-           s.N <= (int64_t)INT32_MAX;
+    return dt == VMB_BF16 && s.d < 128 && tmap_supported() && s.N <= (int64_t)INT32_MAX;
 }
 Shape padded_shape(const Shape& s) {
     Shape p = s;
@@ -1081,19 +976,19 @@ vmb_status vmb_vmonarch_fwd_multi(int32_t n_dev, const int32_t* devices, vmb_sha
         const int64_t es = dtype == VMB_BF16 ? 2 : 4;
         // K is gathered on the call's stream; V, first needed by the last R half-step, on a side
         // stream per device, so its transfer overlaps the first R and L half-steps
-        std::vector<OverlapStreams*> side(n_dev);
+        std::vector<SideStream*> side(n_dev);
         for (int r = 0; r < n_dev; ++r) {
             const MultiPart& p = parts[r];
             VMB_CHECK_CUDA(cudaSetDevice(devices[r]));
-            side[r] = &overlap_streams();
+            side[r] = &side_stream();
             uint8_t* base = static_cast<uint8_t*>(workspace[r]);
             VMB_CHECK_CUDA(cudaEventRecord(side[r]->fork, st[r]));
-            VMB_CHECK_CUDA(cudaStreamWaitEvent(side[r]->chain, side[r]->fork, 0));
+            VMB_CHECK_CUDA(cudaStreamWaitEvent(side[r]->st, side[r]->fork, 0));
             peer_gather(k, v, base + p.fwd_bytes, base + p.fwd_bytes + p.kv_bytes, p.s.U, p.s.T, p.s.hw,
                         p.s.d * es, n_dev, off.data(), cnt.data(), st[r], 1);
             peer_gather(k, v, base + p.fwd_bytes, base + p.fwd_bytes + p.kv_bytes, p.s.U, p.s.T, p.s.hw,
-                        p.s.d * es, n_dev, off.data(), cnt.data(), side[r]->chain, 2);
-            VMB_CHECK_CUDA(cudaEventRecord(side[r]->join, side[r]->chain));
+                        p.s.d * es, n_dev, off.data(), cnt.data(), side[r]->st, 2);
+            VMB_CHECK_CUDA(cudaEventRecord(side[r]->join, side[r]->st));
         }
         join_streams(n_dev, devices, st);  // no device's K input is reused before every peer read it
         for (int r = 0; r < n_dev; ++r) {
@@ -1220,7 +1115,7 @@ vmb_status vmb_rstep(int64_t units, int64_t m, int64_t b, int64_t d, vmb_dtype d
         if (tc) {
             Tc2Args f2{};
             f2.tmQ = internal_map(aR, units, m, b, d, true, 128, 1);
-            f2.tmK = internal_map(Kb, units, m, b, d, true, attn_kv_box(true), 1);
+            f2.tmK = internal_map(Kb, units, m, b, d, true, kRstepKvBox, 1);
             f2.tmV = f2.tmK;
             f2.nseg = (int32_t)m;
             f2.q_len = f2.kv_len = (int32_t)b;
@@ -1237,9 +1132,7 @@ vmb_status vmb_rstep(int64_t units, int64_t m, int64_t b, int64_t d, vmb_dtype d
             int32_t* dummy = nullptr;
             scratch_alloc(reinterpret_cast<void**>(&dummy), sizeof(int32_t), st);
             f2.status = dummy;
-            QRows qv;
-            qv.base = aR; qv.B = m * b * d; qv.H = 0; qv.S = b * d; qv.R = d; qv.Hn = 1;
-            attn_launch(f2, units, st, true, qv);
+            tc2_fa_launch(f2, units, st);
             VMB_CHECK_CUDA(cudaFreeAsync(dummy, st));
             return;
         }
@@ -1354,13 +1247,12 @@ vmb_status vmb_flash_entropy_fwd(int64_t units, int64_t nq, int64_t nk, int64_t 
         VMB_REQUIRE_DOMAIN(nk >= 1, "attention over empty keys");
         cudaStream_t st = as_stream(stream);
         const bool bf16 = dtype == VMB_BF16;
-        // entropy needs the fa3 family (the default); other A/B families run it on CUDA cores
-        const bool tc = bf16 && d == 128 && (ent == nullptr || attn_impl(false) == 3) && tmap_supported() &&
+        const bool tc = bf16 && d == 128 && tmap_supported() &&
                         aligned16(q) && aligned16(k) && aligned16(v) && aligned16(o) && nq <= INT32_MAX &&
                         nk <= INT32_MAX;
         if (tc) {
             Tc2Args f2{};
-            const uint32_t bn = attn_kv_box(false);
+            const uint32_t bn = kAttnKvBox;
             const uint64_t sq = (uint64_t)(nq * d * 2), sk = (uint64_t)(nk * d * 2);
             const uint64_t dq[5] = {(uint64_t)d, (uint64_t)nq, 1, 1, (uint64_t)std::max<int64_t>(units, 1)};
             const uint64_t dk[5] = {(uint64_t)d, (uint64_t)nk, 1, 1, (uint64_t)std::max<int64_t>(units, 1)};
@@ -1396,7 +1288,7 @@ vmb_status vmb_flash_entropy_fwd(int64_t units, int64_t nq, int64_t nk, int64_t 
                 f2.max_split = 1;
             }
             f2.status = dummy;
-            attn_launch(f2, units, st, false);
+            tc3_fa_launch(f2, units, st);
             if (part) VMB_CHECK_CUDA(cudaFreeAsync(part, st));
             VMB_CHECK_CUDA(cudaFreeAsync(dummy, st));
             return;
@@ -1426,13 +1318,9 @@ vmb_status vmb_flash_entropy_bwd(int64_t units, int64_t nq, int64_t nk, int64_t 
         VMB_REQUIRE_DIM(units * nq == 0 || (q && o && dout && lse && dq), "null tensor pointer");
         VMB_REQUIRE_DIM(k && v && dk && dv, "null tensor pointer");
         cudaStream_t st = as_stream(stream);
-        // tcgen05 kernels for bf16 / d = 128 (VMB_BWD=simt forces the CUDA-core kernels)
-        static const bool force_simt = [] {
-            const char* e = getenv("VMB_BWD");
-            return e && std::strcmp(e, "simt") == 0;
-        }();
+        // tcgen05 kernels for bf16 / d = 128, CUDA-core kernels otherwise
         auto al32 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31) == 0; };
-        if (!force_simt && dtype == VMB_BF16 && d == 128 && units > 0 && nq > 0 && tmap_supported() &&
+        if (dtype == VMB_BF16 && d == 128 && units > 0 && nq > 0 && tmap_supported() &&
             aligned16(q) && aligned16(k) && aligned16(v) && aligned16(o) && aligned16(dout) && al32(dq) && al32(dk) &&
             al32(dv)) {
             void* rowstat = nullptr;

@@ -72,6 +72,20 @@ def gather_slabs(x_local, grid, group=None):
     return recv.view(world, U, grid.t_frames, smax, d), parts, smax
 
 
+_SIDE_STREAMS: dict = {}
+
+
+def _side_stream(device):
+    """One V-gather stream per device, reused by every call (streams are not free to create)."""
+    import torch
+
+    key = device.index
+    st = _SIDE_STREAMS.get(key)
+    if st is None:
+        st = _SIDE_STREAMS[key] = torch.cuda.Stream(device=device)
+    return st
+
+
 def vmonarch_attention_seq(q_local, k_local, v_local, grid, cfg=None, group=None):
     """Sequence-sharded VMonarch forward: every rank holds the slab
     slab_partition(h*w, world)[rank] of all frames for Q, K, V; K and V are all-gathered over
@@ -93,7 +107,7 @@ def vmonarch_attention_seq(q_local, k_local, v_local, grid, cfg=None, group=None
     k_full = vm.seq_assemble(kg, grid, begins, counts)
     # V on a side stream: first read by the last R half-step, so its all-gather overlaps the
     # first R and L half-steps (every rank issues K then V: the same collective order)
-    side = torch.cuda.Stream(device=q_local.device)
+    side = _side_stream(q_local.device)
     side.wait_stream(main)
     with torch.cuda.stream(side):
         vg, _, _ = gather_slabs(v_local, grid, group)

@@ -111,7 +111,7 @@ def test_workspace_size(vm):
     c = vm.VMonarchConfig()
     n = g.tokens() * 40
     ws = vm._vmb_ws_size(C.byref(g._c()), C.byref(c._c()), 1)
-    base = 3 * n * 128 * 2 + 2 * n * 4  # aR, aL, y (bf16) + cR, cL (f32)
+    base = 4 * n * 128 * 2 + 2 * n * 4  # aR, aL, aL_lo, y (bf16) + cR, cL (f32)
     split_kv = 40 * 16 * (28 * 52) * 129 * 4  # recompute split-KV partials, at most 16 splits
     assert base <= ws <= base + split_kv + 8 * 256
 
