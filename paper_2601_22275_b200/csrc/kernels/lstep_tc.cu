@@ -143,6 +143,9 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
         float amax = 0.f;
 #pragma unroll
         for (int k = 0; k < NCH * 32; ++k) amax = (k < m) ? fmaxf(amax, fabsf(s[k])) : amax;
+        // TMEM lanes t >= m hold don't-care rows (the M = 128 MMA reads past Qb's R rows into
+        // whatever shared memory follows): they must not steer the gate
+        if (t >= m) amax = 0.f;
         tc_fence_before();
         if (__syncthreads_or(amax * a.qscale > kLstepLoGate)) {
             if (leader) {

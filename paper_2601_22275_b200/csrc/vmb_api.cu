@@ -218,6 +218,9 @@ Shape make_shape(const vmb_grid* g, const vmb_config* c) {
     return s;
 }
 
+#ifndef VMB_DISABLE_LO
+#define VMB_DISABLE_LO 0
+#endif
 struct Workspace {
     int32_t* status;
     void* aR;
@@ -245,7 +248,7 @@ Workspace carve(void* base, const Shape& s, vmb_dtype dt) {
     w.aL = p + off; off += act;
     w.y = p + off; off += act;
     w.aL_lo = nullptr;
-    if (dt == VMB_BF16 && s.d == 128 && s.m <= 128) {
+    if (dt == VMB_BF16 && s.d == 128 && s.m <= 128 && !VMB_DISABLE_LO) {
         w.aL_lo = p + off;
         off += act;
     }
