@@ -40,8 +40,21 @@ tb = (C.c_longlong * (16 * 2 * 12 * 6))()
 vm.lib.vmb_debug_trace4t_read.argtypes = [C.c_void_p]
 vm.lib.vmb_debug_trace4t_read(C.addressof(tb))
 tt = np.frombuffer(tb, dtype=np.int64).reshape(16, 2, 12, 6).astype(np.float64)
-ph = ["wait S", "TMEM ld", "max+xchg", "exp/P st", "st wait+arrive"]
+ph = ["wait S", "TMEM ld", "max", "exp/P st", "st wait+arrive"]
 d = np.diff(tt, axis=3)[:, :, 1:11]  # tiles 1..10
 print("softmax tile phases (cycles, mean over CTAs/items/tiles):", {ph[i]: round(float(d[..., i].mean())) for i in range(5)})
 per = np.diff(tt[:, :, :, 0], axis=2)[:, :, 1:10]
 print("softmax tile period (cycles):", round(float(per.mean())))
+
+# MMA issuer waits (clock64 cycles), tiles 24..47 of the first 16 CTAs
+tm = (C.c_longlong * (16 * 24 * 4))()
+vm.lib.vmb_debug_trace4m_read.argtypes = [C.c_void_p]
+vm.lib.vmb_debug_trace4m_read(C.addressof(tm))
+m = np.frombuffer(tm, dtype=np.int64).reshape(16, 24, 4).astype(np.float64)
+print("MMA issuer per tile (cycles): kv_full wait", round(float((m[:, :, 1] - m[:, :, 0]).mean())),
+      " p_full wait", round(float((m[:, :, 3] - m[:, :, 2]).mean())),
+      " tile period", round(float(np.diff(m[:, :, 0], axis=1).mean())))
+print("MMA issuer per tile (cycles): S issue+commit", round(float((m[:, :, 2] - m[:, :, 1]).mean())),
+      " PV issue+commit", round(float((m[:, 1:, 0] - m[:, :-1, 3]).mean())))
+print("per-tile samples CTA0:", [(int(m[0, i, 1] - m[0, i, 0]), int(m[0, i, 2] - m[0, i, 1]), int(m[0, i, 3] - m[0, i, 2]),
+                                  int(m[0, i + 1, 0] - m[0, i, 3])) for i in range(12)])
