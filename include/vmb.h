@@ -20,8 +20,11 @@
  *    reference's unit-major layout and BSHD activations are accepted).  NULL means
  *    contiguous unit-major: unit u = b*H + h at offset u*N*d, token stride d.
  *  - dtype VMB_F32: fp32 storage and fp32/f64 arithmetic mirroring the reference
- *    precision policy (parity mode, <= 1e-4).  VMB_BF16: bf16 storage, tcgen05 bf16
- *    tensor-core math with fp32 accumulation and fp32 row statistics (<= 2e-2).
+ *    precision policy for T = float (parity mode, <= 1e-4).  VMB_F64: the same on f64
+ *    storage and arithmetic, the reference's T = double (video.hpp:84 is a template over
+ *    T; its tests run in double); vmb_vmonarch_fwd and vmb_export_factors only.
+ *    VMB_BF16: bf16 storage, tcgen05 bf16 tensor-core math with fp32 accumulation and fp32
+ *    row statistics (<= 2e-2).
  *  - Errors mirror check.hpp:10-20: VMB_ERR_DIM (std::invalid_argument "dimension
  *    error"), VMB_ERR_DOMAIN (std::domain_error), VMB_ERR_STATE (std::logic_error).
  *    Host-detectable errors are returned synchronously; data-dependent domain
@@ -50,7 +53,7 @@ typedef enum {
     VMB_ERR_NCCL = 5     /* collective failure (sequence-sharded mode)    */
 } vmb_status;
 
-typedef enum { VMB_F32 = 0, VMB_BF16 = 1 } vmb_dtype;
+typedef enum { VMB_F32 = 0, VMB_BF16 = 1, VMB_F64 = 2 } vmb_dtype;
 
 /* TokenGrid (video.hpp:16-27): frame-major tokens, token = t*(h*w) + r*w + c. */
 typedef struct {
@@ -102,7 +105,8 @@ vmb_status vmb_workspace_status(void* workspace, void* stream);
 
 /* Factor export (MonarchFactors, monarch.hpp:12-19) for the most recent
  * vmb_vmonarch_fwd that used `workspace`: L (units, b, m, m) and R (units, m, b, b)
- * in fp32 (device pointers; either may be NULL), recomputed from the workspace state with
+ * in fp32 -- f64 for dtype VMB_F64, the buffers passed cast to float* -- (device pointers;
+ * either may be NULL), recomputed from the workspace state with
  * the same q/k the forward used.  Call R before or together with L (the L export reuses
  * the aR/cR scratch).  Small N only: R is m*b*b per unit. */
 vmb_status vmb_export_factors(const vmb_grid* grid, const vmb_config* cfg, vmb_dtype dtype,

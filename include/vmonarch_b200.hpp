@@ -20,10 +20,12 @@
 // clamp_enabled, recompute_first_frame, override_m_b}).  `threads` is accepted for
 // signature parity (all units run in one stream-ordered device call).
 //
-// Host buffers are copied to the device, the forward runs in the fp32 parity mode (CUDA
-// cores, the reference precision policy; <= 1e-4 vs the reference) for T = float, and the
-// result is copied back.  Device-resident bf16 callers use the C ABI directly
-// (vmb_vmonarch_fwd with VMB_BF16: the tcgen05 path).  Errors are thrown as
+// Host buffers stream through the device in chunks of batch*head units (pinned staging,
+// H2D / forward / D2H overlapped on three CUDA streams).  The forward runs in the fp32 parity
+// mode (CUDA cores, the reference precision policy; <= 1e-4 vs the reference) for T = float,
+// in the f64 mode for T = double (agreement to round-off, as the reference's double tests
+// need), or with the trailing Precision::bf16 on the tcgen05 path.  Device-resident bf16
+// callers use the C ABI directly (vmb_vmonarch_fwd with VMB_BF16).  Errors are thrown as
 // std::invalid_argument ("dimension error: ..."), std::domain_error ("domain error: ..."),
 // std::logic_error ("state error: ...") or std::runtime_error (CUDA failures).
 #pragma once
@@ -121,6 +123,8 @@ std::pair<int64_t, int64_t> factorize(const GridT& grid, const CfgT& cfg) {
 // ---------------------------------------------------------------- host <-> device helpers
 template <class MatT>
 DeviceBuffer to_device(const MatT& m) {
+    static_assert(std::is_same_v<std::remove_cv_t<std::remove_reference_t<decltype(m.data[0])>>, float>,
+                  "flash_entropy_fwd / _bwd / dense_forward take T = float matrices");
     DeviceBuffer b((size_t)m.rows * m.cols * sizeof(float));
     if (b.size()) check_cuda(cudaMemcpy(b.get(), m.data.data(), b.size(), cudaMemcpyHostToDevice), "H2D");
     return b;
@@ -242,16 +246,87 @@ inline float bf16_to_f32(uint16_t h) {
 }
 }  // namespace detail
 
+namespace detail {
+// Pinned host staging and device buffers of the pipelined host path, kept per thread and
+// grown on demand (page-locking gigabytes per call would cost more than the copies).
+struct PinnedBuffer {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void reserve(size_t n) {
+        if (n <= bytes) return;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+        check_cuda(cudaHostAlloc(&p, n, cudaHostAllocDefault), "cudaHostAlloc");
+        bytes = n;
+    }
+    ~PinnedBuffer() {
+        if (p) cudaFreeHost(p);
+    }
+};
+struct HostPipeline {
+    PinnedBuffer in[2], out[2];
+    cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+    cudaEvent_t h2d_done[2] = {}, comp_done[2] = {}, d2h_done[2] = {};
+    int device = -1;
+    void init() {
+        int dev = 0;
+        check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+        if (device == dev) return;
+        release();
+        device = dev;
+        check_cuda(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking), "stream");
+        check_cuda(cudaStreamCreateWithFlags(&comp, cudaStreamNonBlocking), "stream");
+        check_cuda(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking), "stream");
+        for (int i = 0; i < 2; ++i) {
+            check_cuda(cudaEventCreateWithFlags(&h2d_done[i], cudaEventDisableTiming), "event");
+            check_cuda(cudaEventCreateWithFlags(&comp_done[i], cudaEventDisableTiming), "event");
+            check_cuda(cudaEventCreateWithFlags(&d2h_done[i], cudaEventDisableTiming), "event");
+        }
+    }
+    void release() {
+        if (device < 0) return;
+        cudaStreamDestroy(h2d);
+        cudaStreamDestroy(comp);
+        cudaStreamDestroy(d2h);
+        for (int i = 0; i < 2; ++i) {
+            cudaEventDestroy(h2d_done[i]);
+            cudaEventDestroy(comp_done[i]);
+            cudaEventDestroy(d2h_done[i]);
+        }
+        device = -1;
+    }
+    ~HostPipeline() { release(); }
+};
+inline HostPipeline& host_pipeline() {
+    static thread_local HostPipeline p;
+    p.init();
+    return p;
+}
+}  // namespace detail
+
+// video.hpp:84-150 for host matrices.  T = float runs the fp32 parity mode (Precision::fp32,
+// <= 1e-4 of the reference) or, with Precision::bf16, the tcgen05 path; T = double runs the f64
+// mode (the reference's T = double, CUDA cores, agreement to round-off).
+//
+// Host path: batch*head units are independent (video.hpp:115-148; per-unit results are
+// bitwise independent of how units are grouped), so they stream through the device in
+// chunks of `chunk_units` on three CUDA streams -- host staging into pinned memory, H2D,
+// forward and D2H of consecutive chunks overlap (double-buffered pinned and device buffers).
+// With factors_out the call runs as one chunk (the factor export reads the forward's state).
 template <class MatT, class GridT, class CfgT, class FactorsVec = std::vector<int>>
 std::vector<MatT> vmonarch_attention(std::span<const MatT> qs, std::span<const MatT> ks, std::span<const MatT> vs,
                                      const GridT& grid, const CfgT& cfg, int threads = 1,
-                                     FactorsVec* factors_out = nullptr, Precision prec = Precision::fp32) {
+                                     FactorsVec* factors_out = nullptr, Precision prec = Precision::fp32,
+                                     int64_t chunk_units = 0) {
     (void)threads;
     using T = typename std::remove_cv_t<std::remove_reference_t<decltype(qs[0].data[0])>>;
-    static_assert(std::is_same_v<T, float>, "the drop-in façade takes the reference's T = float matrices");
+    static_assert(std::is_same_v<T, float> || std::is_same_v<T, double>,
+                  "the drop-in façade takes the reference's T = float or T = double matrices");
+    constexpr bool f64 = std::is_same_v<T, double>;
     const bool bf16 = prec == Precision::bf16;
-    const vmb_dtype dt = bf16 ? VMB_BF16 : VMB_F32;
-    const size_t es = bf16 ? 2 : 4;
+    const vmb_dtype dt = bf16 ? VMB_BF16 : (f64 ? VMB_F64 : VMB_F32);
+    const size_t es = bf16 ? 2 : sizeof(T);
     const int64_t units = (int64_t)grid.heads * (int64_t)grid.batch;
     check_dim((int64_t)qs.size() == units && (int64_t)ks.size() == units && (int64_t)vs.size() == units,
               "expected one Q/K/V matrix per batch*head unit");
@@ -264,58 +339,122 @@ std::vector<MatT> vmonarch_attention(std::span<const MatT> qs, std::span<const M
     const vmb_config c = to_config(cfg);
     int64_t m = 0, b = 0;
     check(vmb_factorize(&g, &c, &m, &b));
-
-    const size_t unit_elems = (size_t)n * d, unit_bytes = unit_elems * es;
-    DeviceBuffer dq(unit_bytes * units), dk(unit_bytes * units), dv(unit_bytes * units), dout(unit_bytes * units);
-    std::vector<uint16_t> stage(bf16 ? unit_elems : 0);
-    auto upload = [&](const MatT& m, void* dst, const char* what) {
-        const void* src = m.data.data();
-        if (bf16) {
-            for (size_t x = 0; x < unit_elems; ++x) stage[x] = detail::f32_to_bf16(m.data[x]);
-            src = stage.data();
-        }
-        check_cuda(cudaMemcpy(dst, src, unit_bytes, cudaMemcpyHostToDevice), what);
-    };
-    for (int64_t u = 0; u < units; ++u) {
-        upload(qs[u], (char*)dq.get() + u * unit_bytes, "H2D q");
-        upload(ks[u], (char*)dk.get() + u * unit_bytes, "H2D k");
-        upload(vs[u], (char*)dv.get() + u * unit_bytes, "H2D v");
-    }
-    const size_t ws_bytes = vmb_workspace_size(&g, &c, dt);
-    if (ws_bytes == 0) raise_status(VMB_ERR_DIM);
-    DeviceBuffer ws(ws_bytes);
-    check(vmb_vmonarch_fwd(&g, &c, dt, dq.get(), dk.get(), dv.get(), dout.get(), nullptr, nullptr, ws.get(), ws_bytes,
-                           nullptr));
-    check(vmb_workspace_status(ws.get(), nullptr));  // device-raised domain errors (monarch.hpp:44, 78)
-
     std::vector<MatT> out;
-    out.reserve((size_t)units);
-    for (int64_t u = 0; u < units; ++u) {
-        out.emplace_back(n, d);
-        void* dst = bf16 ? (void*)stage.data() : (void*)out.back().data.data();
-        check_cuda(cudaMemcpy(dst, (char*)dout.get() + u * unit_bytes, unit_bytes, cudaMemcpyDeviceToHost),
-                   "D2H out");
-        if (bf16)
-            for (size_t x = 0; x < unit_elems; ++x) out.back().data[x] = detail::bf16_to_f32(stage[x]);
+    if (units == 0) return out;
+
+    const bool want_factors = [&] {
+        if constexpr (!std::is_same_v<FactorsVec, std::vector<int>>) return factors_out != nullptr;
+        return false;
+    }();
+    const size_t unit_elems = (size_t)n * d, unit_bytes = unit_elems * es;
+    // default: ~8 chunks (the pipeline depth that hides the copies), at most 512 MB per tensor chunk
+    int64_t chunk = chunk_units > 0 ? chunk_units : std::max<int64_t>(1, (units + 7) / 8);
+    chunk = std::min<int64_t>(chunk, std::max<int64_t>(1, (int64_t)((size_t(512) << 20) / std::max<size_t>(unit_bytes, 1))));
+    if (want_factors) chunk = units;
+    chunk = std::min(chunk, units);
+    const int64_t n_chunks = (units + chunk - 1) / chunk;
+
+    vmb_grid gc = g;  // a chunk: `cu` contiguous units, unit-major
+    gc.heads = chunk;
+    gc.batch = 1;
+    const size_t ws_bytes = vmb_workspace_size(&gc, &c, dt);
+    if (ws_bytes == 0) raise_status(VMB_ERR_DIM);
+    const size_t chunk_bytes = (size_t)chunk * unit_bytes;
+    DeviceBuffer dev_in[2] = {DeviceBuffer(3 * chunk_bytes), DeviceBuffer(n_chunks > 1 ? 3 * chunk_bytes : 0)};
+    DeviceBuffer dev_out[2] = {DeviceBuffer(chunk_bytes), DeviceBuffer(n_chunks > 1 ? chunk_bytes : 0)};
+    DeviceBuffer ws[2] = {DeviceBuffer(ws_bytes), DeviceBuffer(n_chunks > 1 ? ws_bytes : 0)};
+    // the device status word of each chunk's forward (vmb.h: workspace offset 0), parked in a
+    // 256-byte status-only "workspace" so vmb_workspace_status can interpret it
+    DeviceBuffer status(2 * 256);
+    detail::HostPipeline& hp = detail::host_pipeline();
+    for (int s2 = 0; s2 < 2; ++s2) {
+        hp.in[s2].reserve(3 * chunk_bytes);
+        hp.out[s2].reserve(chunk_bytes);
     }
+    out.reserve((size_t)units);
+    for (int64_t u = 0; u < units; ++u) out.emplace_back(n, d);
+
+    auto stage_in = [&](const MatT& mtx, uint8_t* dst) {
+        if (bf16) {
+            uint16_t* h = reinterpret_cast<uint16_t*>(dst);
+            for (size_t x = 0; x < unit_elems; ++x) h[x] = detail::f32_to_bf16((float)mtx.data[x]);
+        } else {
+            std::memcpy(dst, mtx.data.data(), unit_bytes);
+        }
+    };
+    auto unstage_out = [&](const uint8_t* src, MatT& mtx) {
+        if (bf16) {
+            const uint16_t* h = reinterpret_cast<const uint16_t*>(src);
+            for (size_t x = 0; x < unit_elems; ++x) mtx.data[x] = (T)detail::bf16_to_f32(h[x]);
+        } else {
+            std::memcpy(mtx.data.data(), src, unit_bytes);
+        }
+    };
+    auto drain = [&](int64_t ci) {
+        const int sl = (int)(ci % 2);
+        const int64_t u0 = ci * chunk, cu = std::min(chunk, units - u0);
+        check_cuda(cudaEventSynchronize(hp.d2h_done[sl]), "D2H");
+        check(vmb_workspace_status((uint8_t*)status.get() + sl * 256, hp.d2h));  // monarch.hpp:44, 78
+        const uint8_t* src = static_cast<const uint8_t*>(hp.out[sl].p);
+        for (int64_t u = 0; u < cu; ++u) unstage_out(src + u * unit_bytes, out[(size_t)(u0 + u)]);
+    };
+    for (int64_t ci = 0; ci < n_chunks; ++ci) {
+        const int sl = (int)(ci % 2);
+        const int64_t u0 = ci * chunk, cu = std::min(chunk, units - u0);
+        // slot sl's pinned input staging is free once chunk ci-2's H2D has landed
+        if (ci >= 2) check_cuda(cudaEventSynchronize(hp.h2d_done[sl]), "H2D");
+        uint8_t* hin = static_cast<uint8_t*>(hp.in[sl].p);
+        for (int64_t u = 0; u < cu; ++u) {
+            stage_in(qs[u0 + u], hin + u * unit_bytes);
+            stage_in(ks[u0 + u], hin + chunk_bytes + u * unit_bytes);
+            stage_in(vs[u0 + u], hin + 2 * chunk_bytes + u * unit_bytes);
+        }
+        uint8_t* din = static_cast<uint8_t*>(dev_in[sl].get());
+        if (ci >= 2) check_cuda(cudaStreamWaitEvent(hp.h2d, hp.comp_done[sl], 0), "wait");  // device inputs reusable
+        for (int t = 0; t < 3; ++t)
+            check_cuda(cudaMemcpyAsync(din + t * chunk_bytes, hin + t * chunk_bytes, (size_t)cu * unit_bytes,
+                                       cudaMemcpyHostToDevice, hp.h2d), "H2D");
+        check_cuda(cudaEventRecord(hp.h2d_done[sl], hp.h2d), "event");
+        check_cuda(cudaStreamWaitEvent(hp.comp, hp.h2d_done[sl], 0), "wait");
+        if (ci >= 2) check_cuda(cudaStreamWaitEvent(hp.comp, hp.d2h_done[sl], 0), "wait");  // device output reusable
+        vmb_grid gci = gc;
+        gci.heads = cu;
+        check(vmb_vmonarch_fwd(&gci, &c, dt, din, din + chunk_bytes, din + 2 * chunk_bytes, dev_out[sl].get(),
+                               nullptr, nullptr, ws[sl].get(), ws_bytes, hp.comp));
+        check_cuda(cudaMemcpyAsync((uint8_t*)status.get() + sl * 256, ws[sl].get(), sizeof(int32_t),
+                                   cudaMemcpyDeviceToDevice, hp.comp), "status");
+        check_cuda(cudaEventRecord(hp.comp_done[sl], hp.comp), "event");
+        // the host drains chunk ci-1 (freeing pinned output slot 1-sl) while chunk ci computes
+        if (ci >= 1) drain(ci - 1);
+        check_cuda(cudaStreamWaitEvent(hp.d2h, hp.comp_done[sl], 0), "wait");
+        check_cuda(cudaMemcpyAsync(hp.out[sl].p, dev_out[sl].get(), (size_t)cu * unit_bytes, cudaMemcpyDeviceToHost,
+                                   hp.d2h), "D2H");
+        check_cuda(cudaEventRecord(hp.d2h_done[sl], hp.d2h), "event");
+    }
+    drain(n_chunks - 1);
+
     if constexpr (!std::is_same_v<FactorsVec, std::vector<int>>) {
         if (factors_out) {
-            // MonarchFactors (monarch.hpp:12-19): L (b, m, m), R (m, b, b) per unit
-            DeviceBuffer dL((size_t)units * b * m * m * sizeof(float)), dR((size_t)units * m * b * b * sizeof(float));
-            check(vmb_export_factors(&g, &c, dt, dq.get(), dk.get(), nullptr, ws.get(), (float*)dL.get(),
-                                     (float*)dR.get(), nullptr));
-            check_cuda(cudaDeviceSynchronize(), "factor export");
+            // MonarchFactors (monarch.hpp:12-19): L (b, m, m), R (m, b, b) per unit, in the
+            // state type of the mode (T = double: double)
+            using S = std::conditional_t<f64, double, float>;
+            DeviceBuffer dL((size_t)units * b * m * m * sizeof(S)), dR((size_t)units * m * b * b * sizeof(S));
+            uint8_t* din = static_cast<uint8_t*>(dev_in[0].get());
+            check(vmb_export_factors(&g, &c, dt, din, din + chunk_bytes, nullptr, ws[0].get(), (float*)dL.get(),
+                                     (float*)dR.get(), hp.comp));
+            check_cuda(cudaStreamSynchronize(hp.comp), "factor export");
             factors_out->resize((size_t)units);
+            std::vector<S> hL((size_t)b * m * m), hR((size_t)m * b * b);
             for (int64_t u = 0; u < units; ++u) {
                 auto& f = (*factors_out)[(size_t)u];
                 f.L = decltype(f.L)(b, m, m);
                 f.R = decltype(f.R)(m, b, b);
-                check_cuda(cudaMemcpy(f.L.data.data(), (float*)dL.get() + (size_t)u * b * m * m,
-                                      (size_t)b * m * m * sizeof(float), cudaMemcpyDeviceToHost),
-                           "D2H L");
-                check_cuda(cudaMemcpy(f.R.data.data(), (float*)dR.get() + (size_t)u * m * b * b,
-                                      (size_t)m * b * b * sizeof(float), cudaMemcpyDeviceToHost),
-                           "D2H R");
+                check_cuda(cudaMemcpy(hL.data(), (S*)dL.get() + (size_t)u * b * m * m, hL.size() * sizeof(S),
+                                      cudaMemcpyDeviceToHost), "D2H L");
+                check_cuda(cudaMemcpy(hR.data(), (S*)dR.get() + (size_t)u * m * b * b, hR.size() * sizeof(S),
+                                      cudaMemcpyDeviceToHost), "D2H R");
+                for (size_t x = 0; x < hL.size(); ++x) f.L.data[x] = hL[x];
+                for (size_t x = 0; x < hR.size(); ++x) f.R.data[x] = hR[x];
             }
         }
     }

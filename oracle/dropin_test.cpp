@@ -23,19 +23,21 @@
 
 using vmonarch::Mat;
 
-static std::vector<Mat<float>> randn_units(int units, long rows, long cols, uint64_t seed, double sigma) {
-    std::vector<Mat<float>> out;
+template <class T = float>
+static std::vector<Mat<T>> randn_units(int units, long rows, long cols, uint64_t seed, double sigma) {
+    std::vector<Mat<T>> out;
     for (int u = 0; u < units; ++u) {
         std::mt19937_64 rng(seed + 3 * u);
         std::normal_distribution<double> nd(0.0, 1.0);
-        Mat<float> m(rows, cols);
-        for (auto& x : m.data) x = static_cast<float>(sigma * nd(rng));
+        Mat<T> m(rows, cols);
+        for (auto& x : m.data) x = static_cast<T>(sigma * nd(rng));
         out.push_back(std::move(m));
     }
     return out;
 }
 
-static double relfro(const std::vector<float>& a, const std::vector<float>& b) {
+template <class T>
+static double relfro(const std::vector<T>& a, const std::vector<T>& b) {
     double num = 0, den = 0;
     for (size_t i = 0; i < a.size(); ++i) {
         num += (double(a[i]) - b[i]) * (double(a[i]) - b[i]);
@@ -105,6 +107,77 @@ int main() {
     parity_case("clamp disabled, sigma=2", vmonarch::TokenGrid{3, 6, 5, 32, 3, 1}, noclamp, 2.0, false);
     parity_case("batch 2 x heads 2, d=16", vmonarch::TokenGrid{5, 4, 4, 16, 2, 2}, vmonarch::VMonarchConfig{}, 3.0,
                 false);
+
+    // T = double (the reference's own tests run in double): the f64 mode, agreement to round-off
+    {
+        struct DCase {
+            const char* name;
+            vmonarch::TokenGrid g;
+            int iters;
+            bool recompute;
+            double sigma;
+        };
+        for (const DCase& dc : {DCase{"f64 C1 t=3", {4, 8, 8, 64, 2, 1}, 3, true, 1.0},
+                                DCase{"f64 3x6x5 d=32 sigma=3", {3, 6, 5, 32, 3, 1}, 2, true, 3.0},
+                                DCase{"f64 5x4x4 d=16 batch 2, no recompute", {5, 4, 4, 16, 2, 2}, 2, false, 1.0}}) {
+            const long n = dc.g.tokens();
+            auto qs = randn_units<double>((int)dc.g.units(), n, dc.g.head_dim, 300, dc.sigma);
+            auto ks = randn_units<double>((int)dc.g.units(), n, dc.g.head_dim, 301, dc.sigma);
+            auto vs = randn_units<double>((int)dc.g.units(), n, dc.g.head_dim, 302, dc.sigma);
+            std::span<const Mat<double>> sq(qs), sk(ks), sv(vs);
+            vmonarch::VMonarchConfig cf;
+            cf.iters = dc.iters;
+            cf.recompute_first_frame = dc.recompute;
+            std::vector<vmonarch::MonarchFactors<double>> fr, fg;
+            auto ref = vmonarch::vmonarch_attention<double>(sq, sk, sv, dc.g, cf, 4, &fr);
+            auto got = vmonarch_b200::vmonarch_attention(sq, sk, sv, dc.g, cf, 4, &fg);
+            double worst = 0, wl = 0, wr = 0;
+            for (size_t u = 0; u < ref.size(); ++u) {
+                worst = std::max(worst, relfro(got[u].data, ref[u].data));
+                wl = std::max(wl, relfro(fg[u].L.data, fr[u].L.data));
+                wr = std::max(wr, relfro(fg[u].R.data, fr[u].R.data));
+            }
+            char buf[240];
+            std::snprintf(buf, sizeof buf, "%s: output rel-Fro %.2e, factors L %.2e R %.2e (<= 1e-11)", dc.name, worst,
+                          wl, wr);
+            expect(got.size() == ref.size() && worst <= 1e-11 && wl <= 1e-11 && wr <= 1e-11, buf);
+        }
+    }
+
+    // the pipelined host path: units streamed in chunks (1 and 3 units) equal the one-chunk call
+    // bitwise, and equal the reference
+    {
+        vmonarch::TokenGrid g{4, 8, 16, 128, 7, 1};
+        const long n = g.tokens();
+        auto qs = randn_units((int)g.units(), n, 128, 400, 1.0);
+        auto ks = randn_units((int)g.units(), n, 128, 401, 1.0);
+        auto vs = randn_units((int)g.units(), n, 128, 402, 1.0);
+        std::span<const Mat<float>> sq(qs), sk(ks), sv(vs);
+        vmonarch::VMonarchConfig cf;
+        std::vector<vmonarch::MonarchFactors<float>>* none = nullptr;
+        for (auto prec : {vmonarch_b200::Precision::fp32, vmonarch_b200::Precision::bf16}) {
+            auto whole = vmonarch_b200::vmonarch_attention(sq, sk, sv, g, cf, 1, none, prec, 7);
+            bool same = true;
+            for (int64_t ch : {1, 3}) {
+                auto part = vmonarch_b200::vmonarch_attention(sq, sk, sv, g, cf, 1, none, prec, ch);
+                for (size_t u = 0; u < whole.size(); ++u) same = same && part[u].data == whole[u].data;
+            }
+            auto ref = vmonarch::vmonarch_attention<float>(sq, sk, sv, g, cf, 4);
+            double worst = 0;
+            for (size_t u = 0; u < ref.size(); ++u) worst = std::max(worst, relfro(whole[u].data, ref[u].data));
+            const bool bf = prec == vmonarch_b200::Precision::bf16;
+            char buf[200];
+            std::snprintf(buf, sizeof buf, "%s host pipeline, chunks of 1/3/7 units: bitwise equal %s, rel-Fro %.2e",
+                          bf ? "bf16" : "fp32", same ? "yes" : "NO", worst);
+            expect(same && worst <= (bf ? 2e-2 : 1e-4), buf);
+        }
+        // a non-finite Q in the last chunk is still reported
+        qs[6].data[3] = NAN;
+        expect(throws<std::domain_error>([&] {
+                   vmonarch_b200::vmonarch_attention(sq, sk, sv, g, cf, 1, none, vmonarch_b200::Precision::bf16, 2);
+               }),
+               "host pipeline: non-finite Q in the last chunk -> std::domain_error");
+    }
 
     // bf16 performance mode of the façade (Precision::bf16): float in / float out on the tcgen05 path
     {

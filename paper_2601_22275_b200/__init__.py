@@ -124,7 +124,7 @@ _vmb_fwd_multi = _sig("vmb_vmonarch_fwd_multi", [_I32, _P, C.c_int, C.POINTER(_G
                       + [_P] * 7)
 _vmb_selftest = _sig("vmb_selftest_umma", [_I32, _P, _P, _P, _P])
 
-VMB_F32, VMB_BF16 = 0, 1
+VMB_F32, VMB_BF16, VMB_F64 = 0, 1, 2
 _ERRORS = {1: DimensionError, 2: DomainError, 3: StateError, 4: CudaError, 5: CudaError}
 
 
@@ -226,9 +226,11 @@ def make_perm(b: int, n: int) -> list:
 def _dtype_code(t: torch.Tensor) -> int:
     if t.dtype == torch.float32:
         return VMB_F32
+    if t.dtype == torch.float64:
+        return VMB_F64
     if t.dtype == torch.bfloat16:
         return VMB_BF16
-    raise DimensionError(f"dimension error: unsupported dtype {t.dtype} (float32 or bfloat16)")
+    raise DimensionError(f"dimension error: unsupported dtype {t.dtype} (bfloat16, float32 or float64)")
 
 
 def _stream(device: Optional[torch.device] = None) -> C.c_void_p:
@@ -335,7 +337,8 @@ def vmonarch_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, grid: 
     """video.hpp:84-150 on the GPU.
 
     q, k, v: CUDA tensors (units, N, d) [unit u = b*H + h], or (B, H, N, d) views (BSHD
-    activations pass as ``x.transpose(1, 2)``), float32 (parity mode) or bfloat16.
+    activations pass as ``x.transpose(1, 2)``), float32 (parity mode), float64 (the
+    reference's T = double, CUDA cores) or bfloat16 (tcgen05).
     Returns O with the layout of ``q`` (3-D) or a (B, H, N, d) tensor.
     ``factors_out``: if a list, receives per-unit (L (b,m,m), R (m,b,b)) fp32 tensors (small N).
     ``check``: synchronise and raise DomainError for device-detected domain errors
@@ -380,8 +383,9 @@ def vmonarch_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, grid: 
         if factors_out is not None:
             m, b = factorize(grid, cfg)
             U = grid.units()
-            L = torch.empty((U, b, m, m), dtype=torch.float32, device=dev)
-            R = torch.empty((U, m, b, b), dtype=torch.float32, device=dev)
+            fdt = torch.float64 if dt == VMB_F64 else torch.float32  # the state type of the mode
+            L = torch.empty((U, b, m, m), dtype=fdt, device=dev)
+            R = torch.empty((U, m, b, b), dtype=fdt, device=dev)
             _check(_vmb_export(C.byref(g), C.byref(c), dt, _ptr(q), _ptr(k), C.byref(sq), _ptr(ws), _ptr(L),
                                _ptr(R), st))
             factors_out.clear()
@@ -392,7 +396,8 @@ def vmonarch_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, grid: 
 def workspace_size(grid: TokenGrid, cfg: VMonarchConfig = VMonarchConfig(), dtype=torch.bfloat16) -> int:
     """Bytes of scratch one vmonarch_attention call needs (vmb_workspace_size)."""
     g, c = grid._c(), cfg._c()
-    n = int(_vmb_ws_size(C.byref(g), C.byref(c), VMB_BF16 if dtype == torch.bfloat16 else VMB_F32))
+    code = {torch.bfloat16: VMB_BF16, torch.float32: VMB_F32, torch.float64: VMB_F64}[dtype]
+    n = int(_vmb_ws_size(C.byref(g), C.byref(c), code))
     if n == 0:
         _check(1)
     return n
@@ -617,8 +622,9 @@ def export_factors(q, k, grid, cfg, dtype_code):
     """Factor export for the last vmonarch_attention call on this device (MonarchFactors)."""
     m, b = factorize(grid, cfg)
     U = grid.units()
-    L = torch.empty((U, b, m, m), dtype=torch.float32, device=q.device)
-    R = torch.empty((U, m, b, b), dtype=torch.float32, device=q.device)
+    fdt = torch.float64 if dtype_code == VMB_F64 else torch.float32
+    L = torch.empty((U, b, m, m), dtype=fdt, device=q.device)
+    R = torch.empty((U, m, b, b), dtype=fdt, device=q.device)
     stream = torch.cuda.current_stream(q.device)
     ws = _workspace(grid, cfg, dtype_code, q.device, stream)
     g, c = grid._c(), cfg._c()

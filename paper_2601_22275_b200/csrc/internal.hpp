@@ -86,52 +86,54 @@ CUtensorMap make_tmap_bf16_5d(const void* base, const uint64_t dims[5],
 bool tmap_supported();
 
 // ---------------------------------------------------------------- SIMT kernels (any dtype)
+// CUDA-core kernels (simt.cu).  State pointers (cR, cL, R, L, part_acc) hold the compute type:
+// float for VMB_F32 / VMB_BF16, double for VMB_F64.
 struct SimtRstepArgs {
     View A;            // query rows (u, k, i): aR or Q
-    float qscale;      // multiplies the logits
-    const float* cR;   // (U, m, b) or nullptr (== 1)
-    float clamp_min;
+    double qscale;     // multiplies the logits (rounded to the compute type in the kernel)
+    const void* cR;    // (U, m, b) or nullptr (== 1)
+    double clamp_min;
     int clamp_enabled;
     View K;            // key rows (u, k, l)
     View V;            // value rows (u, k, l)
     View Out;          // output rows (u, k, i)  (aL or y)
-    float* cL;         // (U, b, m) or nullptr
-    float* R;          // (U, m, b, b) or nullptr
+    void* cL;          // (U, b, m) or nullptr
+    void* R;           // (U, m, b, b) or nullptr
     int64_t U, m, b, d;
     int32_t* status;
 };
 struct SimtLstepArgs {
     View Q;            // Qb rows (u, i, j)
-    float qscale;
+    double qscale;
     View aL;           // rows (u, i, k)
-    const float* cL;   // (U, b, m)
+    const void* cL;    // (U, b, m)
     View aR;           // ITER: output rows (u, k, i)
-    float* cR;         // ITER: (U, m, b)
+    void* cR;          // ITER: (U, m, b)
     View Y;            // FINAL: rows (u, k, i)
     View O;            // FINAL: output rows (u, j, i)
     int32_t skip_j0;   // FINAL: rows j == 0 are produced elsewhere (recompute)
-    float* L;          // (U, b, m, m) or nullptr
+    void* L;           // (U, b, m, m) or nullptr
     int32_t final_mode;
     int64_t U, m, b, d;
 };
 struct SimtFlashArgs {
     View Q;            // rows (u, 0, r), r < nq
-    float qscale;
+    double qscale;
     View K, V;         // rows (u, 0, l), l < nk
     View O;            // rows (u, 0, r)
-    float* lse;        // (U, nq) or nullptr
-    float* ent;        // (U, nq) or nullptr
+    float* lse;        // (U, nq) or nullptr (VMB_F32 / VMB_BF16 only)
+    float* ent;        // (U, nq) or nullptr (VMB_F32 / VMB_BF16 only)
     int64_t U, nq, nk, d;
     // split-KV (set by simt_flash): key range split `blockIdx.z` of `nsplit`; partial rows
     // (unnormalised acc, fp32) and statistics (max, sum, entropy accumulator; double)
     int32_t nsplit = 1;
-    float* part_acc = nullptr;     // (nsplit, U, nq, d)
+    void* part_acc = nullptr;      // (nsplit, U, nq, d), compute type
     double* part_stat = nullptr;   // (nsplit, U, nq, 3)
 };
-void simt_rstep(const SimtRstepArgs& a, bool bf16, cudaStream_t s);
-void simt_lstep(const SimtLstepArgs& a, bool bf16, cudaStream_t s);
-void simt_flash(const SimtFlashArgs& a, bool bf16, cudaStream_t s);
-void check_finite_rows(View q, int64_t U, int64_t rows, int64_t d, bool bf16, int32_t* status,
+void simt_rstep(const SimtRstepArgs& a, vmb_dtype dt, cudaStream_t s);
+void simt_lstep(const SimtLstepArgs& a, vmb_dtype dt, cudaStream_t s);
+void simt_flash(const SimtFlashArgs& a, vmb_dtype dt, cudaStream_t s);
+void check_finite_rows(View q, int64_t U, int64_t rows, int64_t d, vmb_dtype dt, int32_t* status,
                        cudaStream_t s);
 void check_clamp_domain(const float* cR, int64_t n, int32_t* status, cudaStream_t s);
 

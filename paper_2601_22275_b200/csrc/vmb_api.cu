@@ -221,6 +221,8 @@ Shape make_shape(const vmb_grid* g, const vmb_config* c) {
 #ifndef VMB_DISABLE_LO
 #define VMB_DISABLE_LO 0
 #endif
+size_t dtype_bytes(vmb_dtype dt) { return dt == VMB_BF16 ? 2 : dt == VMB_F64 ? 8 : 4; }
+
 struct Workspace {
     int32_t* status;
     void* aR;
@@ -237,9 +239,10 @@ struct Workspace {
 };
 
 Workspace carve(void* base, const Shape& s, vmb_dtype dt) {
-    const size_t es = dt == VMB_BF16 ? 2 : 4;
+    const size_t es = dtype_bytes(dt);
     const size_t act = align_up((size_t)s.U * s.Nq * s.d * es);
-    const size_t st = align_up((size_t)s.U * s.Nq * sizeof(float));
+    // half-step state (cR, cL, lse2) in the compute type: float, double for VMB_F64
+    const size_t st = align_up((size_t)s.U * s.Nq * (dt == VMB_F64 ? sizeof(double) : sizeof(float)));
     uint8_t* p = static_cast<uint8_t*>(base);
     Workspace w;
     w.status = reinterpret_cast<int32_t*>(p);
@@ -372,7 +375,6 @@ cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q, const void* k,
              const void* v, void* o, const vmb_strides& in, const vmb_strides& kin, const vmb_strides& out,
              const Workspace& ws, cudaStream_t st, cudaEvent_t v_ready = nullptr) {
-    const bool bf16 = dt == VMB_BF16;
     const float qscale = (float)(1.0 / std::sqrt((double)(s.d_real > 0 ? s.d_real : s.d)));
     const bool recompute = cfg.recompute_first_frame != 0;
     const bool skip_j0 = recompute && s.b == s.hw;
@@ -556,7 +558,8 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
     // ---------------------------------------------------- CUDA-core path (any shape / fp32)
     VMB_REQUIRE_DIM(!sharded, "the sequence-sharded mode needs the tcgen05 path (bf16, d = 128, m <= 128)");
     if (v_ready) VMB_CHECK_CUDA(cudaStreamWaitEvent(st, v_ready, 0));
-    check_finite_rows(user_view(q, in, s, 0, 1), U, s.N, d, bf16, ws.status, st);
+    check_finite_rows(user_view(q, in, s, 0, 1), U, s.N, d, dt, ws.status, st);
+    const double qscale_d = 1.0 / std::sqrt((double)(s.d_real > 0 ? s.d_real : s.d));  // in the compute type
     const View vQrow = user_view(q, in, s, b, 1);    // (u, k, i) -> token k*b+i
     const View vK = user_view(k, in, s, b, 1);
     const View vV = user_view(v, in, s, b, 1);
@@ -570,9 +573,9 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
         const bool last = t == cfg.iters - 1;
         SimtRstepArgs ra{};
         ra.A = t == 0 ? vQrow : vAR;
-        ra.qscale = t == 0 ? qscale : 1.f;
+        ra.qscale = t == 0 ? qscale_d : 1.0;
         ra.cR = t == 0 ? nullptr : ws.cR;
-        ra.clamp_min = (float)cfg.clamp_min;
+        ra.clamp_min = cfg.clamp_min;
         ra.clamp_enabled = cfg.clamp_enabled;
         ra.K = vK;
         ra.V = vK;
@@ -581,16 +584,16 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
         ra.R = nullptr;
         ra.U = U; ra.m = m; ra.b = b; ra.d = d;
         ra.status = ws.status;
-        simt_rstep(ra, bf16, st);
+        simt_rstep(ra, dt, st);
         if (last) {  // y = R V with the same R (monarch.hpp:182-185)
             ra.V = vV;
             ra.Out = vY;
             ra.cL = nullptr;
-            simt_rstep(ra, bf16, st);
+            simt_rstep(ra, dt, st);
         }
         SimtLstepArgs la{};
         la.Q = vQcol;
-        la.qscale = qscale;
+        la.qscale = qscale_d;
         la.aL = vAL_in;
         la.cL = ws.cL;
         la.aR = vAR;
@@ -602,19 +605,19 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
         la.L = nullptr;
         la.final_mode = last;
         la.U = U; la.m = m; la.b = b; la.d = d;
-        simt_lstep(la, bf16, st);
+        simt_lstep(la, dt, st);
     }
     if (recompute) {
         SimtFlashArgs fa{};
         fa.Q = user_view(q, in, s, 0, 1);
-        fa.qscale = qscale;
+        fa.qscale = qscale_d;
         fa.K = user_view(k, in, s, 0, 1);
         fa.V = user_view(v, in, s, 0, 1);
         fa.O = user_view(o, out, s, 0, 1);
         fa.lse = nullptr;
         fa.ent = nullptr;
         fa.U = U; fa.nq = s.hw; fa.nk = s.N; fa.d = d;
-        simt_flash(fa, bf16, st);
+        simt_flash(fa, dt, st);
     }
 }
 
@@ -732,7 +735,7 @@ vmb_status vmb_vmonarch_fwd(const vmb_grid* grid, const vmb_config* cfg, vmb_dty
                             const vmb_strides* out_strides, void* workspace, size_t ws_bytes, void* stream) {
     return guarded([&] {
         const Shape s = make_shape(grid, cfg);
-        VMB_REQUIRE_DIM(dtype == VMB_F32 || dtype == VMB_BF16, "unsupported dtype");
+        VMB_REQUIRE_DIM(dtype == VMB_F32 || dtype == VMB_BF16 || dtype == VMB_F64, "unsupported dtype");
         vmb_strides ti, to;
         const vmb_strides* in = or_default(in_strides, ti, s);
         const vmb_strides* out = or_default(out_strides, to, s);
@@ -1043,7 +1046,7 @@ vmb_status vmb_export_factors(const vmb_grid* grid, const vmb_config* cfg, vmb_d
         Shape s = make_shape(grid, cfg);
         vmb_strides ti;
         const vmb_strides* in = or_default(in_strides, ti, s);
-        const float qscale = (float)(1.0 / std::sqrt((double)s.d));
+        VMB_REQUIRE_DIM(dtype == VMB_F32 || dtype == VMB_BF16 || dtype == VMB_F64, "unsupported dtype");
         if (padded_path(s, dtype)) {
             // the forward ran on the zero-padded copies it left in the workspace
             const Shape p = padded_shape(s);
@@ -1054,8 +1057,9 @@ vmb_status vmb_export_factors(const vmb_grid* grid, const vmb_config* cfg, vmb_d
             ti = default_strides(p);
             in = &ti;
         }
+        // the forward's softmax scale: the real head dim, also on the zero-padded path
+        const double qscale = 1.0 / std::sqrt((double)(s.d_real > 0 ? s.d_real : s.d));
         const Workspace ws = carve(workspace, s, dtype);
-        const bool bf16 = dtype == VMB_BF16;
         cudaStream_t st = as_stream(stream);
         const int64_t m = s.m, b = s.b, d = s.d, ud = m * b * d;
         if (R) {
@@ -1064,9 +1068,9 @@ vmb_status vmb_export_factors(const vmb_grid* grid, const vmb_config* cfg, vmb_d
             SimtRstepArgs ra{};
             const bool first = cfg->iters == 1;
             ra.A = first ? user_view(q, *in, s, b, 1) : internal_view(ws.aR, ud, b * d, d);
-            ra.qscale = first ? qscale : 1.f;
+            ra.qscale = first ? qscale : 1.0;
             ra.cR = first ? nullptr : ws.cR;
-            ra.clamp_min = (float)cfg->clamp_min;
+            ra.clamp_min = cfg->clamp_min;
             ra.clamp_enabled = cfg->clamp_enabled;
             ra.K = user_view(k, *in, s, b, 1);
             ra.V = ra.K;
@@ -1075,7 +1079,7 @@ vmb_status vmb_export_factors(const vmb_grid* grid, const vmb_config* cfg, vmb_d
             ra.R = R;
             ra.U = s.U; ra.m = m; ra.b = b; ra.d = d;
             ra.status = ws.status;
-            simt_rstep(ra, bf16, st);
+            simt_rstep(ra, dtype, st);
         }
         if (L) {
             // L of the last L half-step from (Q, aL, cL); aR/cR are overwritten (scratch).
@@ -1089,7 +1093,7 @@ vmb_status vmb_export_factors(const vmb_grid* grid, const vmb_config* cfg, vmb_d
             la.L = L;
             la.final_mode = 0;
             la.U = s.U; la.m = m; la.b = b; la.d = d;
-            simt_lstep(la, bf16, st);
+            simt_lstep(la, dtype, st);
         }
     });
 }
@@ -1098,6 +1102,7 @@ vmb_status vmb_rstep(int64_t units, int64_t m, int64_t b, int64_t d, vmb_dtype d
                      const float* cR, const void* Kb, double clamp_min, int32_t clamp_enabled, void* aL, float* cL,
                      float* R, void* stream) {
     return guarded([&] {
+        VMB_REQUIRE_DIM(dtype == VMB_F32 || dtype == VMB_BF16, "unsupported dtype (VMB_F64: vmb_vmonarch_fwd only)");
         VMB_REQUIRE_DIM(units >= 0 && m >= 1 && b >= 1 && d >= 1, "factor sizes must be >= 1");
         cudaStream_t st = as_stream(stream);
         const bool bf16 = dtype == VMB_BF16;
@@ -1143,9 +1148,9 @@ vmb_status vmb_rstep(int64_t units, int64_t m, int64_t b, int64_t d, vmb_dtype d
         scratch_alloc(reinterpret_cast<void**>(&dummy), sizeof(int32_t), st);
         SimtRstepArgs ra{};
         ra.A = internal_view(aR, ud, b * d, d);
-        ra.qscale = 1.f;
+        ra.qscale = 1.0;
         ra.cR = cR;
-        ra.clamp_min = (float)clamp_min;
+        ra.clamp_min = clamp_min;
         ra.clamp_enabled = clamp_enabled;
         ra.K = internal_view(Kb, ud, b * d, d);
         ra.V = ra.K;
@@ -1154,7 +1159,7 @@ vmb_status vmb_rstep(int64_t units, int64_t m, int64_t b, int64_t d, vmb_dtype d
         ra.R = R;
         ra.U = units; ra.m = m; ra.b = b; ra.d = d;
         ra.status = dummy;
-        simt_rstep(ra, bf16, st);
+        simt_rstep(ra, dtype, st);
         VMB_CHECK_CUDA(cudaFreeAsync(dummy, st));
     });
 }
@@ -1162,6 +1167,7 @@ vmb_status vmb_rstep(int64_t units, int64_t m, int64_t b, int64_t d, vmb_dtype d
 vmb_status vmb_lstep(int64_t units, int64_t m, int64_t b, int64_t d, vmb_dtype dtype, const void* Qb,
                      const void* aL, const float* cL, void* aR, float* cR, float* L, void* stream) {
     return guarded([&] {
+        VMB_REQUIRE_DIM(dtype == VMB_F32 || dtype == VMB_BF16, "unsupported dtype (VMB_F64: vmb_vmonarch_fwd only)");
         VMB_REQUIRE_DIM(units >= 0 && m >= 1 && b >= 1 && d >= 1, "factor sizes must be >= 1");
         // l_update needs the aL / cL of a preceding r_update (check_state, monarch.hpp:111)
         if (units > 0 && (aL == nullptr || cL == nullptr))
@@ -1230,7 +1236,7 @@ vmb_status vmb_lstep(int64_t units, int64_t m, int64_t b, int64_t d, vmb_dtype d
         }
         SimtLstepArgs la{};
         la.Q = internal_view(Qb, ud, m * d, d);  // (U,b,m,d) rows (u, i, j)
-        la.qscale = 1.f;
+        la.qscale = 1.0;
         la.aL = internal_view(aL, ud, m * d, d);
         la.cL = cL;
         la.aR = internal_view(aR, ud, b * d, d);
@@ -1238,7 +1244,7 @@ vmb_status vmb_lstep(int64_t units, int64_t m, int64_t b, int64_t d, vmb_dtype d
         la.L = L;
         la.final_mode = 0;
         la.U = units; la.m = m; la.b = b; la.d = d;
-        simt_lstep(la, bf16, st);
+        simt_lstep(la, dtype, st);
     });
 }
 
@@ -1246,6 +1252,7 @@ vmb_status vmb_flash_entropy_fwd(int64_t units, int64_t nq, int64_t nk, int64_t 
                                  const void* k, const void* v, float q_scale, void* o, float* lse, float* ent,
                                  void* stream) {
     return guarded([&] {
+        VMB_REQUIRE_DIM(dtype == VMB_F32 || dtype == VMB_BF16, "unsupported dtype (VMB_F64: vmb_vmonarch_fwd only)");
         VMB_REQUIRE_DIM(units >= 0 && nq >= 0 && d >= 1, "bad attention shape");
         VMB_REQUIRE_DOMAIN(nk >= 1, "attention over empty keys");
         cudaStream_t st = as_stream(stream);
@@ -1305,7 +1312,7 @@ vmb_status vmb_flash_entropy_fwd(int64_t units, int64_t nq, int64_t nk, int64_t 
         fa.lse = lse;
         fa.ent = ent;
         fa.U = units; fa.nq = nq; fa.nk = nk; fa.d = d;
-        simt_flash(fa, bf16, st);
+        simt_flash(fa, dtype, st);
     });
 }
 
