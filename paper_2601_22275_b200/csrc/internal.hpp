@@ -136,6 +136,9 @@ void simt_flash(const SimtFlashArgs& a, vmb_dtype dt, cudaStream_t s);
 void check_finite_rows(View q, int64_t U, int64_t rows, int64_t d, vmb_dtype dt, int32_t* status,
                        cudaStream_t s);
 void check_clamp_domain(const float* cR, int64_t n, int32_t* status, cudaStream_t s);
+// hilo.cu: x = hi + lo, hi = bf16(x), lo = bf16(x - hi) for the fp32 rows (u, 0, t) of `v`
+// (t < rows), into contiguous (U, rows, d) bf16 tensors; d % 4 == 0, rows 16-byte aligned
+void split_hilo(const View& v, int64_t U, int64_t rows, int64_t d, void* hi, void* lo, cudaStream_t s);
 
 // ---------------------------------------------------------------- tcgen05 kernels (bf16, d = 128)
 // fa2_tc.cu: 2 CTAs/SM flash attention with one value operand (R half-step: value = key,
@@ -169,6 +172,13 @@ struct Tc2Args {
     // optional low half of the bf16 output (R half-step: aL = hi + lo, hi = bf16(aL),
     // lo = bf16(aL - hi)), same layout as `out`; nullptr = not written
     void* out_lo;
+    // fp32 parity mode on tensor cores (hilo = 1): every operand is a pair of bf16 tensors
+    // x = hi + lo; tmQ/tmK/tmV map the hi halves, these the lo halves (same boxes).  Products
+    // run as three bf16 MMA groups (hi hi + hi lo + lo hi) into fp32.  out_f32: `out` rows are
+    // fp32 (strides in floats), else bf16.
+    CUtensorMap tmQlo, tmKlo, tmVlo;
+    int32_t hilo;
+    int32_t out_f32;
 };
 int tc2_kv_tile(int nv);
 // 32-byte alignment of every bf16 output row of an attention launch (256-bit epilogue stores)

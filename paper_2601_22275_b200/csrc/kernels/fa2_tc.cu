@@ -99,14 +99,20 @@ __device__ __forceinline__ uint64_t ex2_emu2(uint64_t x2) {
 
 constexpr int kBN = 64;  // keys per KV tile (S tile = 128 x 64, double-buffered in TMEM)
 
-template <int NB>
+// HL (the fp32 parity mode on tensor cores): every operand X arrives as two bf16 tensors
+// X = hi + lo (hi = bf16(x), lo = bf16(x - hi): 16 mantissa bits), and each product is three
+// bf16 MMA groups into one fp32 accumulator, A B ~ Ah Bh + Ah Bl + Al Bh (the dropped Al Bl is
+// 2^-16 relative).  P goes to TMEM as hi (S columns [0,32)) and lo ([32,64)).  The lo tiles
+// sit right after their hi tiles in shared memory; 192 KB, so one CTA per SM.
+template <int NB, bool HL>
 struct Smem {
     static constexpr int S = NB == 1 ? 4 : 2;             // KV stages
     static constexpr uint32_t kv_panel = kBN * 128;       // 64 rows x 64 bf16
     static constexpr uint32_t kv_tile = 2 * kv_panel;     // 64 x 128
+    static constexpr uint32_t op_tile = HL ? 2 * kv_tile : kv_tile;  // one operand (hi [+ lo]) per stage
     static constexpr uint32_t q_off = 0;
-    static constexpr uint32_t kv_off = 2 * kQPanel;
-    static constexpr uint32_t bar_off = kv_off + S * NB * kv_tile;
+    static constexpr uint32_t kv_off = (HL ? 4 : 2) * kQPanel;
+    static constexpr uint32_t bar_off = kv_off + S * NB * op_tile;
     // q_full, kv_full[S], kv_empty[S], s_full[2], p_full[2], pv_done, o_full
     static constexpr uint32_t n_bars = 1 + 2 * S + 6;
     static constexpr uint32_t slot_off = bar_off + n_bars * 8;
@@ -114,9 +120,9 @@ struct Smem {
     static constexpr uint32_t alloc = bytes + 1024;
 };
 
-template <int NB>
-__global__ void __launch_bounds__(kThreads, 2) fa2_kernel(const __grid_constant__ Params p) {
-    using SM = Smem<NB>;
+template <int NB, bool HL>
+__global__ void __launch_bounds__(kThreads, HL ? 1 : 2) fa2_kernel(const __grid_constant__ Params p) {
+    using SM = Smem<NB, HL>;
     constexpr int S = SM::S;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
@@ -145,6 +151,11 @@ __global__ void __launch_bounds__(kThreads, 2) fa2_kernel(const __grid_constant_
         tma_prefetch_desc(&a.tmQ);
         tma_prefetch_desc(&a.tmK);
         if (NB == 2) tma_prefetch_desc(&a.tmV);
+        if (HL) {
+            tma_prefetch_desc(&a.tmQlo);
+            tma_prefetch_desc(&a.tmKlo);
+            if (NB == 2) tma_prefetch_desc(&a.tmVlo);
+        }
         mbar_init(q_full, 1);
         for (int s = 0; s < S; ++s) {
             mbar_init(&kv_full[s], 1);
@@ -171,20 +182,28 @@ __global__ void __launch_bounds__(kThreads, 2) fa2_kernel(const __grid_constant_
             const int qb = u / a.qH, qh = u % a.qH;
             const int kb = u / a.kH, kh = u % a.kH;
             uint8_t* sq = smem + SM::q_off;
-            mbar_arrive_expect_tx(q_full, 2 * kQPanel);
+            mbar_arrive_expect_tx(q_full, (HL ? 4 : 2) * kQPanel);
             tma_load_5d(sq, &a.tmQ, q_full, 0, qtile * kQTile, seg, qh, qb);
             tma_load_5d(sq + kQPanel, &a.tmQ, q_full, 64, qtile * kQTile, seg, qh, qb);
+            if (HL) {
+                tma_load_5d(sq + 2 * kQPanel, &a.tmQlo, q_full, 0, qtile * kQTile, seg, qh, qb);
+                tma_load_5d(sq + 3 * kQPanel, &a.tmQlo, q_full, 64, qtile * kQTile, seg, qh, qb);
+            }
             for (int j = 0; j < n_kv; ++j) {
                 const int st = j % S;
                 if (j >= S) mbar_wait_sleep(&kv_empty[st], ((j / S) + 1) & 1);
-                uint8_t* skv = smem + SM::kv_off + st * NB * SM::kv_tile;
+                uint8_t* skv = smem + SM::kv_off + st * NB * SM::op_tile;
                 const int row = (kv_tile0 + j) * kBN;
-                mbar_arrive_expect_tx(&kv_full[st], NB * SM::kv_tile);
-                tma_load_5d(skv, &a.tmK, &kv_full[st], 0, row, seg, kh, kb);
-                tma_load_5d(skv + SM::kv_panel, &a.tmK, &kv_full[st], 64, row, seg, kh, kb);
+                mbar_arrive_expect_tx(&kv_full[st], NB * SM::op_tile);
+                auto load_op = [&](uint8_t* dst, const CUtensorMap* m) {
+                    tma_load_5d(dst, m, &kv_full[st], 0, row, seg, kh, kb);
+                    tma_load_5d(dst + SM::kv_panel, m, &kv_full[st], 64, row, seg, kh, kb);
+                };
+                load_op(skv, &a.tmK);
+                if (HL) load_op(skv + SM::kv_tile, &a.tmKlo);
                 if (NB == 2) {
-                    tma_load_5d(skv + SM::kv_tile, &a.tmV, &kv_full[st], 0, row, seg, kh, kb);
-                    tma_load_5d(skv + SM::kv_tile + SM::kv_panel, &a.tmV, &kv_full[st], 64, row, seg, kh, kb);
+                    load_op(skv + SM::op_tile, &a.tmV);
+                    if (HL) load_op(skv + SM::op_tile + SM::kv_tile, &a.tmVlo);
                 }
             }
         }
@@ -203,12 +222,19 @@ __global__ void __launch_bounds__(kThreads, 2) fa2_kernel(const __grid_constant_
                     const int st = j % S;
                     mbar_wait_sleep(&kv_full[st], (j / S) & 1);
                     tc_fence_after();
-                    const uint32_t kaddr = kv_addr + st * NB * SM::kv_tile;
+                    const uint32_t kaddr = kv_addr + st * NB * SM::op_tile;
                     const uint32_t tS = tS0 + (j & 1) * kBN;
+                    // HL: Qh Kh + Qh Kl + Ql Kh
 #pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) {
-                        umma_ss(tS, sdesc_sw128(q_addr + (kk >> 2) * kQPanel + (kk & 3) * 32, 16, 1024),
-                                sdesc_sw128(kaddr + (kk >> 2) * SM::kv_panel + (kk & 3) * 32, 16, 1024), idS, kk > 0);
+                    for (int gr = 0; gr < (HL ? 3 : 1); ++gr) {
+                        const uint32_t qa = q_addr + (gr == 2 ? 2 * kQPanel : 0);
+                        const uint32_t ka = kaddr + (gr == 1 ? SM::kv_tile : 0);
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk) {
+                            umma_ss(tS, sdesc_sw128(qa + (kk >> 2) * kQPanel + (kk & 3) * 32, 16, 1024),
+                                    sdesc_sw128(ka + (kk >> 2) * SM::kv_panel + (kk & 3) * 32, 16, 1024), idS,
+                                    (gr > 0 || kk > 0) ? 1u : 0u);
+                        }
                     }
                     umma_commit(&s_full[j & 1]);
                 }
@@ -216,12 +242,18 @@ __global__ void __launch_bounds__(kThreads, 2) fa2_kernel(const __grid_constant_
                     const int jp = j - 1, st = jp % S;
                     mbar_wait_sleep(&p_full[jp & 1], (jp >> 1) & 1);
                     tc_fence_after();
-                    const uint32_t vaddr = kv_addr + st * NB * SM::kv_tile + (NB == 2 ? SM::kv_tile : 0);
+                    const uint32_t vaddr = kv_addr + st * NB * SM::op_tile + (NB == 2 ? SM::op_tile : 0);
                     const uint32_t tP = tS0 + (jp & 1) * kBN;
+                    // HL: Ph Vh + Ph Vl + Pl Vh (P lo in the S buffer's columns [32, 64))
 #pragma unroll
-                    for (int kk = 0; kk < kBN / 16; ++kk) {
-                        umma_ts(tO, tP + kk * 8, sdesc_sw128(vaddr + kk * 2048, SM::kv_panel, 1024), idPV,
-                                (jp > 0 || kk > 0) ? 1u : 0u);
+                    for (int gr = 0; gr < (HL ? 3 : 1); ++gr) {
+                        const uint32_t pa = tP + (gr == 2 ? kBN / 2 : 0);
+                        const uint32_t va = vaddr + (gr == 1 ? SM::kv_tile : 0);
+#pragma unroll
+                        for (int kk = 0; kk < kBN / 16; ++kk) {
+                            umma_ts(tO, pa + kk * 8, sdesc_sw128(va + kk * 2048, SM::kv_panel, 1024), idPV,
+                                    (jp > 0 || gr > 0 || kk > 0) ? 1u : 0u);
+                        }
                     }
                     umma_commit(&kv_empty[st]);
                     umma_commit(pv_done);
@@ -336,9 +368,20 @@ __global__ void __launch_bounds__(kThreads, 2) fa2_kernel(const __grid_constant_
                     default: acc3 = fadd2(acc3, pp); break;
                 }
                 pk[x] = pack_bf16(p0, p1);
+                if (HL) reinterpret_cast<uint64_t*>(sr)[x] = pp;  // s is dead: keep p for the lo half
             }
             VMB_TMEM_ST16(tS + 0, (pk + 0));
             VMB_TMEM_ST16(tS + 16, (pk + 16));
+            if (HL) {
+                // P lo = bf16(p - bf16(p)) over the S columns [32, 64) (already in registers)
+#pragma unroll
+                for (int x = 0; x < kBN / 2; ++x) {
+                    const uint64_t pp = reinterpret_cast<const uint64_t*>(sr)[x];
+                    pk[x] = pack_bf16_residual(lo2(pp), hi2(pp), pk[x]);
+                }
+                VMB_TMEM_ST16(tS + 32, (pk + 0));
+                VMB_TMEM_ST16(tS + 48, (pk + 16));
+            }
             const uint64_t acc = fadd2(fadd2(acc0, acc1), fadd2(acc2, acc3));
             l_run += lo2(acc) + hi2(acc);
             if (rescale) {
@@ -403,19 +446,46 @@ __global__ void __launch_bounds__(kThreads, 2) fa2_kernel(const __grid_constant_
                 VMB_TMEM_LD32(tO + cc * 32 + lane_base, orr);
                 tmem_ld_wait();
                 if (a.cl_out) {
-                    const uint8_t* qp = smem + SM::q_off + (cc >> 1) * kQPanel;
 #pragma unroll
-                    for (int x = 0; x < 4; ++x) {
-                        const uint4 qv = *reinterpret_cast<const uint4*>(qp + sw128_offset(row, (cc & 1) * 32 + 8 * x));
-                        const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
+                    for (int hl = 0; hl < (HL ? 2 : 1); ++hl) {  // HL: q = q_hi + q_lo
+                        const uint8_t* qp = smem + SM::q_off + (2 * hl + (cc >> 1)) * kQPanel;
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            qo = fmaf(__uint_as_float(qw[e] << 16), __uint_as_float(orr[8 * x + 2 * e]), qo);
-                            qo = fmaf(__uint_as_float(qw[e] & 0xFFFF0000u), __uint_as_float(orr[8 * x + 2 * e + 1]), qo);
+                        for (int x = 0; x < 4; ++x) {
+                            const uint4 qv = *reinterpret_cast<const uint4*>(qp + sw128_offset(row, (cc & 1) * 32 + 8 * x));
+                            const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                qo = fmaf(__uint_as_float(qw[e] << 16), __uint_as_float(orr[8 * x + 2 * e]), qo);
+                                qo = fmaf(__uint_as_float(qw[e] & 0xFFFF0000u), __uint_as_float(orr[8 * x + 2 * e + 1]), qo);
+                            }
                         }
                     }
                 }
-                if (valid) {
+                if (HL && a.out_f32) {
+                    // fp32 output rows (element strides in floats)
+                    if (valid) {
+                        float* frow = static_cast<float*>(a.out) + ob * a.oB + oh * a.oH + (int64_t)seg * a.oS +
+                                      (int64_t)grow * a.oR + cc * 32;
+#pragma unroll
+                        for (int x = 0; x < 4; ++x) {
+                            uint4 lo, hi;
+                            lo.x = __float_as_uint(__uint_as_float(orr[8 * x + 0]) * inv_l);
+                            lo.y = __float_as_uint(__uint_as_float(orr[8 * x + 1]) * inv_l);
+                            lo.z = __float_as_uint(__uint_as_float(orr[8 * x + 2]) * inv_l);
+                            lo.w = __float_as_uint(__uint_as_float(orr[8 * x + 3]) * inv_l);
+                            hi.x = __float_as_uint(__uint_as_float(orr[8 * x + 4]) * inv_l);
+                            hi.y = __float_as_uint(__uint_as_float(orr[8 * x + 5]) * inv_l);
+                            hi.z = __float_as_uint(__uint_as_float(orr[8 * x + 6]) * inv_l);
+                            hi.w = __float_as_uint(__uint_as_float(orr[8 * x + 7]) * inv_l);
+                            if (a.out_align32) {
+                                st_global_256(frow + 8 * x, lo, hi);
+                            } else {
+                                reinterpret_cast<uint4*>(frow + 8 * x)[0] = lo;
+                                reinterpret_cast<uint4*>(frow + 8 * x)[1] = hi;
+                            }
+                        }
+                    }
+                } else if (valid) {
                     float f[32];
 #pragma unroll
                     for (int x = 0; x < 32; ++x) f[x] = __uint_as_float(orr[x]) * inv_l;
@@ -522,6 +592,12 @@ __global__ void __launch_bounds__(256) fa2_combine_kernel(const Tc2Args a) {
         a.ent_out[useg * rows + r] = h;
     }
     const int64_t ob = u / a.oHn, oh = u % a.oHn;
+    if (a.out_f32) {
+        float* frow = static_cast<float*>(a.out) + ob * a.oB + oh * a.oH + (int64_t)seg * a.oS + r * a.oR;
+        reinterpret_cast<float4*>(frow)[lane] = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+        if (a.lse_out && lane == 0) a.lse_out[useg * rows + r] = mx + logf(wsum);
+        return;
+    }
     __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(a.out) + ob * a.oB + oh * a.oH + (int64_t)seg * a.oS + r * a.oR;
     uint2 v;
     v.x = pack_bf16(acc.x * inv, acc.y * inv);
@@ -530,10 +606,11 @@ __global__ void __launch_bounds__(256) fa2_combine_kernel(const Tc2Args a) {
     if (a.lse_out && lane == 0) a.lse_out[useg * rows + r] = mx + logf(wsum);
 }
 
-template <int NB>
+template <int NB, bool HL>
 void launch(const Params& p, int64_t n_useg, int nsplit, cudaStream_t s) {
-    using SM = Smem<NB>;
-    auto kern = fa2_kernel<NB>;
+    using SM = Smem<NB, HL>;
+    static_assert(SM::alloc <= 232448, "shared memory budget (227 KB per CTA)");
+    auto kern = fa2_kernel<NB, HL>;
     VMB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM::alloc));
     VMB_REQUIRE_DIM((int64_t)p.q_tiles * nsplit * n_useg <= (int64_t)INT32_MAX, "attention grid too large");
     const dim3 grid((unsigned)((int64_t)p.q_tiles * nsplit * n_useg));
@@ -574,12 +651,21 @@ void tc2_fa_launch(Tc2Args a, int64_t U, cudaStream_t s) {
     p.total_tiles = total_tiles;
     a.nsplit = nsplit;
     a.n_useg = n_useg;
-    a.out_align32 = rows_align32(a.out, a.oB, a.oH, a.oS, a.oR) &&
+    // 32-byte rows: 16 bf16 or 8 fp32 elements per stride unit
+    a.out_align32 = (a.out_f32 ? (reinterpret_cast<uintptr_t>(a.out) % 32 == 0 && a.oB % 8 == 0 && a.oH % 8 == 0 &&
+                                  a.oS % 8 == 0 && a.oR % 8 == 0)
+                               : rows_align32(a.out, a.oB, a.oH, a.oS, a.oR)) &&
                     (!a.out_lo || reinterpret_cast<uintptr_t>(a.out_lo) % 32 == 0) ? 1 : 0;
+    VMB_REQUIRE_DIM(!a.out_f32 || a.hilo, "fp32 output rows need the hi/lo (fp32 parity) instantiation");
     p.a = a;
     if (nsplit == 1) p.a.part_o = nullptr;
-    if (a.nv == 1) launch<1>(p, n_useg, nsplit, s);
-    else launch<2>(p, n_useg, nsplit, s);
+    if (a.hilo) {
+        if (a.nv == 1) launch<1, true>(p, n_useg, nsplit, s);
+        else launch<2, true>(p, n_useg, nsplit, s);
+    } else {
+        if (a.nv == 1) launch<1, false>(p, n_useg, nsplit, s);
+        else launch<2, false>(p, n_useg, nsplit, s);
+    }
     if (nsplit > 1) tc2_combine_launch(p.a, s);
 }
 

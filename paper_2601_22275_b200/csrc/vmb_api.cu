@@ -218,9 +218,6 @@ Shape make_shape(const vmb_grid* g, const vmb_config* c) {
     return s;
 }
 
-#ifndef VMB_DISABLE_LO
-#define VMB_DISABLE_LO 0
-#endif
 size_t dtype_bytes(vmb_dtype dt) { return dt == VMB_BF16 ? 2 : dt == VMB_F64 ? 8 : 4; }
 
 struct Workspace {
@@ -234,9 +231,19 @@ struct Workspace {
     float* part_o;    // split-KV partials of the first-frame recompute (tcgen05 path)
     float* part_lse;
     float* lse2;      // m > 128 (lstep_big.cu): row log-sum-exp of the L-step scores, (U, b, m)
+    // fp32 parity mode on tensor cores: hi/lo bf16 halves of Q, K, V and aR, (U, N, d) each
+    void* qh = nullptr; void* ql = nullptr; void* kh = nullptr; void* kl = nullptr;
+    void* vh = nullptr; void* vl = nullptr; void* arh = nullptr; void* arl = nullptr;
     int nsplit;
     size_t bytes;
 };
+
+// The fp32 parity mode runs on tensor cores (hi/lo bf16 operands, fa2 hilo instantiation)
+// for d = 128 and m <= 128 on the default (unsharded) plan; other fp32 shapes take the
+// CUDA-core kernels.
+bool f32tc_shape(const Shape& s) {
+    return s.d == 128 && s.m <= 128 && s.bq == s.b && s.N <= (int64_t)INT32_MAX && s.d_real == 0 && tmap_supported();
+}
 
 Workspace carve(void* base, const Shape& s, vmb_dtype dt) {
     const size_t es = dtype_bytes(dt);
@@ -251,7 +258,7 @@ Workspace carve(void* base, const Shape& s, vmb_dtype dt) {
     w.aL = p + off; off += act;
     w.y = p + off; off += act;
     w.aL_lo = nullptr;
-    if (dt == VMB_BF16 && s.d == 128 && s.m <= 128 && !VMB_DISABLE_LO) {
+    if (dt == VMB_BF16 && s.d == 128 && s.m <= 128) {
         w.aL_lo = p + off;
         off += act;
     }
@@ -264,6 +271,24 @@ Workspace carve(void* base, const Shape& s, vmb_dtype dt) {
         off += st;
     }
     w.nsplit = 1;
+    if (dt == VMB_F32 && f32tc_shape(s)) {
+        const size_t half = align_up((size_t)s.U * s.N * s.d * 2);
+        void** hl[8] = {&w.qh, &w.ql, &w.kh, &w.kl, &w.vh, &w.vl, &w.arh, &w.arl};
+        for (void** x : hl) {
+            *x = p + off;
+            off += half;
+        }
+        if (s.recompute && s.U > 0) {
+            // fa2 (64-key tiles) split plan of the first-frame recompute
+            w.nsplit = tc2_plan_splits(s.hwq, s.N, s.U, 2, kTc2MaxSplit);
+            if (w.nsplit > 1) {
+                w.part_o = reinterpret_cast<float*>(p + off);
+                off += align_up((size_t)s.U * w.nsplit * s.hwq * 128 * sizeof(float));
+                w.part_lse = reinterpret_cast<float*>(p + off);
+                off += align_up((size_t)s.U * w.nsplit * s.hwq * sizeof(float));
+            }
+        }
+    }
     if (dt == VMB_BF16 && s.d == 128 && s.recompute && s.U > 0) {
         w.nsplit = attn_plan_splits(s.hwq, s.N, s.U);
         if (w.nsplit > 1) {
@@ -551,6 +576,112 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
             } else {
                 tc3_fa_launch(f2, U, st);
             }
+        }
+        return;
+    }
+
+    // ---------------------------------------------------- fp32 parity mode on tensor cores
+    // Q, K, V (and each aR) are split into bf16 hi/lo halves; the R half-steps and the
+    // first-frame recompute run fa2's hilo instantiation (three bf16 MMA groups per product,
+    // fp32 accumulation and statistics, fp32 outputs); the L half-steps (HBM-light at fp32,
+    // ~1% of the FLOPs) run on the CUDA-core kernels.  The last R half-step computes aL and y
+    // in two passes over the same softmax (value = K, then V): fa2 holds one value operand.
+    bool f32tc = dt == VMB_F32 && ws.qh != nullptr && aligned16(q) && aligned16(k) && aligned16(v) && aligned16(o);
+    {
+        const int64_t sts[6] = {in.batch, in.head, in.token, kin.batch, kin.head, kin.token};
+        for (int64_t x : sts) f32tc = f32tc && x % 4 == 0;
+    }
+    if (f32tc) {
+        const int32_t Hm = (int32_t)std::max<int64_t>(s.H, 1);
+        const int64_t ud = m * b * d;
+        split_hilo(user_view(q, in, s, 0, 1), U, s.N, d, ws.qh, ws.ql, st);
+        split_hilo(user_view(k, kin, s, 0, 1), U, s.N, d, ws.kh, ws.kl, st);
+        split_hilo(user_view(v, kin, s, 0, 1), U, s.N, d, ws.vh, ws.vl, st);
+        const uint32_t bn = (uint32_t)tc2_kv_tile(1);
+        const CUtensorMap mQh = internal_map(ws.qh, U, m, b, d, true, 128, 1), mQl = internal_map(ws.ql, U, m, b, d, true, 128, 1);
+        const CUtensorMap mKh = internal_map(ws.kh, U, m, b, d, true, bn, 1), mKl = internal_map(ws.kl, U, m, b, d, true, bn, 1);
+        const CUtensorMap mVh = internal_map(ws.vh, U, m, b, d, true, bn, 1), mVl = internal_map(ws.vl, U, m, b, d, true, bn, 1);
+        const CUtensorMap mAh = internal_map(ws.arh, U, m, b, d, true, 128, 1), mAl = internal_map(ws.arl, U, m, b, d, true, 128, 1);
+        const View vQcol = user_view(q, in, s, 1, b);    // (u, i, j) -> token j*b+i
+        const View vAR = internal_view(ws.aR, ud, b * d, d);
+        const View vAL_in = internal_view(ws.aL, ud, m * d, d);
+        const View vY = internal_view(ws.y, ud, b * d, d);
+        const double qscale_d = 1.0 / std::sqrt((double)d);
+        for (int64_t t = 0; t < cfg.iters; ++t) {
+            const bool last = t == cfg.iters - 1;
+            Tc2Args f2{};
+            f2.hilo = 1;
+            f2.out_f32 = 1;
+            f2.tmQ = t == 0 ? mQh : mAh;
+            f2.tmQlo = t == 0 ? mQl : mAl;
+            f2.tmK = f2.tmV = mKh;
+            f2.tmKlo = f2.tmVlo = mKl;
+            f2.nseg = (int32_t)m; f2.q_len = (int32_t)b; f2.kv_len = (int32_t)b;
+            f2.qH = f2.kH = f2.oHn = 1;
+            f2.cR = t == 0 ? nullptr : ws.cR;
+            f2.qscale = t == 0 ? qscale : 1.f;
+            f2.clamp_min = (float)cfg.clamp_min; f2.clamp_enabled = cfg.clamp_enabled;
+            f2.nv = 1;
+            f2.out = ws.aL;                       // aL (U, b, m, d) fp32: row (u, k, i)
+            f2.oB = b * m * d; f2.oH = 0; f2.oS = d; f2.oR = m * d;
+            f2.cl_out = ws.cL;
+            f2.status = ws.status;
+            f2.check_finite = t == 0;
+            f2.max_split = 1;
+            tc2_fa_launch(f2, U, st);
+            if (last) {
+                // y = R V (monarch.hpp:182-185), the same softmax rows with V as the value
+                Tc2Args fy = f2;
+                fy.nv = 2;
+                fy.tmV = mVh; fy.tmVlo = mVl;
+                fy.out = ws.y;                    // y (U, m, b, d) fp32: row (u, k, i)
+                fy.oB = m * b * d; fy.oH = 0; fy.oS = b * d; fy.oR = d;
+                fy.cl_out = nullptr;
+                fy.check_finite = 0;
+                tc2_fa_launch(fy, U, st);
+            }
+            SimtLstepArgs la{};
+            la.Q = vQcol;
+            la.qscale = qscale_d;
+            la.aL = vAL_in;
+            la.cL = ws.cL;
+            la.aR = vAR;
+            la.cR = ws.cR;
+            la.Y = vY;
+            la.O = user_view(o, out, s, b, 1);  // (u, j, i) -> token j*b+i
+            la.skip_j0 = skip_j0;
+            la.L = nullptr;
+            la.final_mode = last;
+            la.U = U; la.m = m; la.b = b; la.d = d;
+            simt_lstep(la, dt, st);
+            if (!last) split_hilo(internal_view(ws.aR, m * b * d, 0, d), U, m * b, d, ws.arh, ws.arl, st);
+        }
+        if (recompute) {
+            // first-frame recompute (video.hpp:117-126): Q[0:hw) against all N keys, split over
+            // the keys with an LSE combine writing fp32 O rows [0, hw)
+            Tc2Args fr{};
+            fr.hilo = 1;
+            fr.out_f32 = 1;
+            fr.tmQ = internal_map(ws.qh, U, 1, s.N, d, true, 128, 1);
+            fr.tmQlo = internal_map(ws.ql, U, 1, s.N, d, true, 128, 1);
+            fr.tmK = internal_map(ws.kh, U, 1, s.N, d, true, bn, 1);
+            fr.tmKlo = internal_map(ws.kl, U, 1, s.N, d, true, bn, 1);
+            fr.tmV = internal_map(ws.vh, U, 1, s.N, d, true, bn, 1);
+            fr.tmVlo = internal_map(ws.vl, U, 1, s.N, d, true, bn, 1);
+            fr.nseg = 1;
+            fr.q_len = (int32_t)s.hw;
+            fr.kv_len = (int32_t)s.N;
+            fr.qH = fr.kH = 1;
+            fr.oHn = Hm;
+            fr.qscale = qscale;
+            fr.nv = 2;
+            fr.out = o;
+            fr.oB = out.batch; fr.oH = out.head; fr.oS = 0; fr.oR = out.token;
+            fr.status = ws.status;
+            fr.part_o = ws.part_o;
+            fr.part_lse = ws.part_lse;
+            fr.max_split = ws.part_o ? kTc2MaxSplit : 1;
+            tc2_fa_launch(fr, U, st);
         }
         return;
     }
