@@ -139,6 +139,8 @@ void check_clamp_domain(const float* cR, int64_t n, int32_t* status, cudaStream_
 // hilo.cu: x = hi + lo, hi = bf16(x), lo = bf16(x - hi) for the fp32 rows (u, 0, t) of `v`
 // (t < rows), into contiguous (U, rows, d) bf16 tensors; d % 4 == 0, rows 16-byte aligned
 void split_hilo(const View& v, int64_t U, int64_t rows, int64_t d, void* hi, void* lo, cudaStream_t s);
+// out[e] = hi[e] + lo[e] (fp32 state back from its hi/lo pair; the factor export)
+void merge_hilo(const void* hi, const void* lo, float* out, int64_t n, cudaStream_t s);
 
 // ---------------------------------------------------------------- tcgen05 kernels (bf16, d = 128)
 // fa2_tc.cu: 2 CTAs/SM flash attention with one value operand (R half-step: value = key,
@@ -262,6 +264,26 @@ struct TcLstepArgs {
 // logit error under ~1e-3.
 constexpr float kLstepLoGate = 2.0f;
 void tc_lstep_launch(const TcLstepArgs& a, int64_t U, cudaStream_t s);
+// The fp32 parity mode's L half-step / apply on tensor cores (lstep_tc.cu, lstep_hl_kernel):
+// every operand is a bf16 hi/lo pair (x = hi + lo), each product three bf16 MMA groups into
+// fp32; L is stored as hi/lo; outputs are written from registers: ITER aR as hi/lo bf16
+// (U, m, b, d) rows plus cR, FINAL O as fp32 rows of the caller's tensor.  d = 128, m <= 128.
+struct TcLstepHlArgs {
+    CUtensorMap tmQ, tmQlo;     // Qb rows of the hi/lo copies of Q, (d, i, j, 1, unit), box (64, 1, rows)
+    CUtensorMap tmAL, tmALlo;   // aL hi/lo (d, k, i, 1, unit), box (64, rows, 1)
+    CUtensorMap tmY, tmYlo;     // FINAL: y hi/lo (d, i, k, 1, unit), box (64, 1, rows)
+    const float* cL;            // (U, b, m)
+    float qscale;
+    int32_t m, b;
+    int32_t final_mode;
+    float* cR;                  // ITER: (U, m, b)
+    void* ar_hi;                // ITER: aR * qscale as bf16 hi/lo, (U, m, b, d)
+    void* ar_lo;
+    float* out;                 // FINAL: O row (u, token j*b + i) at (u/oHn)*oB + (u%oHn)*oH + token*oT
+    int64_t oB, oH, oT;
+    int32_t oHn;
+};
+void tc_lstep_hl_launch(const TcLstepHlArgs& a, int64_t U, cudaStream_t s);
 // lstep_big.cu: L half-step / apply for m > 128 (row statistics pass + ITER or FINAL pass)
 struct TcLstepBigArgs {
     CUtensorMap tmQ128, tmQ64;    // Qb rows (d, i, j, head, batch), boxes (64, 1, 128) / (64, 1, 64)

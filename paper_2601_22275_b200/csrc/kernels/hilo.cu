@@ -31,7 +31,22 @@ __global__ void __launch_bounds__(256) split_hilo_kernel(View v, int64_t U, int6
     }
 }
 
+__global__ void __launch_bounds__(256) merge_hilo_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* lo, float* out,
+                                                          int64_t n) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        out[e] = __bfloat162float(hi[e]) + __bfloat162float(lo[e]);
+}
+
 }  // namespace
+
+void merge_hilo(const void* hi, const void* lo, float* out, int64_t n, cudaStream_t s) {
+    if (n == 0) return;
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    merge_hilo_kernel<<<blocks, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(hi), static_cast<const __nv_bfloat16*>(lo),
+                                             out, n);
+    count_launch();
+    check_launch("merge_hilo");
+}
 
 void split_hilo(const View& v, int64_t U, int64_t rows, int64_t d, void* hi, void* lo, cudaStream_t s) {
     const int64_t total = U * rows * (d / 4);

@@ -291,6 +291,281 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
     __syncthreads();
 }
 
+// ------------------------------------------------------------------ fp32 parity mode (hi/lo)
+// The same half-step with every operand a bf16 hi/lo pair (x = hi + lo) and each product
+// three MMA groups, A B ~ Ah Bh + Ah Bl + Al Bh, into the fp32 accumulator (the dropped Al Bl
+// is 2^-16 relative).  Shared memory (P = R*128 bytes per 64-column panel):
+//   [Qb hi: 2P][Qb lo: 2P][aL hi -> L hi: 2P][aL lo -> L lo: 2P][y hi: 2P][y lo: 2P (FINAL)][cL]
+// Outputs leave from registers (thread = row): ITER aR*qscale as hi/lo bf16 rows and cR;
+// FINAL O as fp32 rows.
+struct HlLayout {
+    uint32_t panel, cl, bars, slot, bytes;
+    __host__ __device__ HlLayout(int rows, bool final_mode) {
+        panel = (uint32_t)rows * 128u;
+        cl = (final_mode ? 12 : 8) * panel;
+        bars = cl + 512;
+        slot = bars + 32;
+        bytes = slot + 16;
+        // M = 128 A reads from the last A panel (Qb lo panel 1, or L lo panel 1) stay inside
+        const uint32_t a_end = 7 * panel + 128u * 128u;
+        bytes = bytes > a_end ? bytes : a_end;
+    }
+};
+struct HlParams {
+    TcLstepHlArgs a;
+    int32_t rows;
+};
+
+template <bool FINAL, int NCH>
+__global__ void __launch_bounds__(kThreads, FINAL ? 1 : 2) lstep_hl_kernel(const __grid_constant__ HlParams p) {
+    const TcLstepHlArgs& a = p.a;
+    const int R = p.rows;
+    const HlLayout L(R, FINAL);
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint64_t* bar_load = reinterpret_cast<uint64_t*>(smem + L.bars);
+    uint64_t* bar_mma1 = bar_load + 1;
+    uint64_t* bar_mma2 = bar_load + 2;
+    uint32_t* slot = reinterpret_cast<uint32_t*>(smem + L.slot);
+    float* s_cl = reinterpret_cast<float*>(smem + L.cl);
+    const uint32_t P = L.panel;
+    // operand tiles: q (hi, lo), l (aL -> L; hi, lo), y (hi, lo); each 2 panels
+    const uint32_t base = smem_u32(smem);
+    const uint32_t q_hi = base, q_lo = base + 2 * P, l_hi = base + 4 * P, l_lo = base + 6 * P;
+    const uint32_t y_hi = base + 8 * P, y_lo = base + 10 * P;
+
+    const int i = blockIdx.x, u = blockIdx.y;
+    const int m = a.m;
+    const int warp = warp_id();
+    const int t = threadIdx.x;
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+
+    if (warp == 0) {
+        if (elect_one()) {
+            mbar_init(bar_load, 1);
+            mbar_init(bar_mma1, 1);
+            mbar_init(bar_mma2, 1);
+            fence_mbar_init();
+            mbar_arrive_expect_tx(bar_load, (FINAL ? 12u : 8u) * P);
+            const CUtensorMap* qm[2] = {&a.tmQ, &a.tmQlo};
+            const CUtensorMap* lm[2] = {&a.tmAL, &a.tmALlo};
+            const CUtensorMap* ym[2] = {&a.tmY, &a.tmYlo};
+            for (int h = 0; h < 2; ++h) {
+                tma_load_5d(smem + 2 * h * P, qm[h], bar_load, 0, i, 0, 0, u);
+                tma_load_5d(smem + (2 * h + 1) * P, qm[h], bar_load, 64, i, 0, 0, u);
+                tma_load_5d(smem + (4 + 2 * h) * P, lm[h], bar_load, 0, 0, i, 0, u);
+                tma_load_5d(smem + (5 + 2 * h) * P, lm[h], bar_load, 64, 0, i, 0, u);
+                if (FINAL) {
+                    tma_load_5d(smem + (8 + 2 * h) * P, ym[h], bar_load, 0, i, 0, 0, u);
+                    tma_load_5d(smem + (9 + 2 * h) * P, ym[h], bar_load, 64, i, 0, 0, u);
+                }
+            }
+        }
+        __syncwarp();
+        tmem_alloc<128>(slot);
+    }
+    const float* cl = a.cL + ((int64_t)u * a.b + i) * m;
+    if (t < R) s_cl[t] = (t < m) ? cl[t] : 0.f;
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *slot;
+    const bool leader = (warp == 0) && elect_one();
+
+    if (leader) {
+        // GEMM 1: S = Qb aL^T  (Qh aLh + Qh aLl + Ql aLh)
+        mbar_wait(bar_load, 0);
+        tc_fence_after();
+        const uint32_t id1 = idesc_bf16(128, (uint32_t)R, 0, 0);
+        const uint32_t qa[3] = {q_hi, q_hi, q_lo}, la[3] = {l_hi, l_lo, l_hi};
+#pragma unroll
+        for (int gr = 0; gr < 3; ++gr) {
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                const uint32_t off = (kk >> 2) * P + (kk & 3) * 32;
+                umma_ss(tmem, sdesc_sw128(qa[gr] + off, 16, 1024), sdesc_sw128(la[gr] + off, 16, 1024), id1,
+                        (gr > 0 || kk > 0) ? 1u : 0u);
+            }
+        }
+        umma_commit(bar_mma1);
+    }
+    __syncwarp();
+
+    // ---- softmax of row j = t over k < m   (monarch.hpp:124-138)
+    mbar_wait(bar_mma1, 0);
+    tc_fence_after();
+    uint32_t sr[NCH * 32];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) VMB_TMEM_LD32(tmem + lane_base + c * 32, (sr + c * 32));
+    tmem_ld_wait();
+    float* s = reinterpret_cast<float*>(sr);
+    const float sc2 = a.qscale * kLog2e;
+    float mx = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < NCH * 32; ++k) {
+        s[k] = (k < m) ? (s[k] * sc2 - s_cl[k] * kLog2e) : -INFINITY;
+        mx = fmaxf(mx, s[k]);
+    }
+    float sum = 0.f;
+#pragma unroll
+    for (int k = 0; k < NCH * 32; ++k) {
+        s[k] = (k < m) ? ex2(s[k] - mx) : 0.f;
+        sum += s[k];
+    }
+    // rows j >= m are written as zeros: they are part of GEMM 2's K extent (ITER)
+    const float inv = (t < m) ? 1.f / sum : 0.f;
+    // L row j -> hi/lo bf16, SW128, over the consumed aL hi/lo tiles
+    if (t < R) {
+#pragma unroll
+        for (int c8 = 0; c8 < NCH * 4; ++c8) {
+            if (c8 * 8 < R) {
+                uint4 h, l;
+                float f[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) f[e] = s[8 * c8 + e] * inv;
+                h.x = pack_bf16(f[0], f[1]);
+                h.y = pack_bf16(f[2], f[3]);
+                h.z = pack_bf16(f[4], f[5]);
+                h.w = pack_bf16(f[6], f[7]);
+                l.x = pack_bf16_residual(f[0], f[1], h.x);
+                l.y = pack_bf16_residual(f[2], f[3], h.y);
+                l.z = pack_bf16_residual(f[4], f[5], h.z);
+                l.w = pack_bf16_residual(f[6], f[7], h.w);
+                const uint32_t off = (c8 >> 3) * P + sw128_offset(t, (c8 & 7) * 8);
+                *reinterpret_cast<uint4*>(smem + 4 * P + off) = h;
+                *reinterpret_cast<uint4*>(smem + 6 * P + off) = l;
+            }
+        }
+    }
+    fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    if (leader) {
+        const uint32_t nk = (uint32_t)R / 16;
+        if (!FINAL) {
+            // aR' = L^T Qb: A = L^T (M=k, K=j) MN-major, B = Qb (K=j, N=d) MN-major
+            const uint32_t id2 = idesc_bf16(128, 128, 1, 1);
+            const uint32_t aa[3] = {l_hi, l_hi, l_lo}, bb[3] = {q_hi, q_lo, q_hi};
+#pragma unroll
+            for (int gr = 0; gr < 3; ++gr)
+                for (uint32_t kk = 0; kk < nk; ++kk)
+                    umma_ss(tmem, sdesc_sw128(aa[gr] + kk * 2048, P, 1024), sdesc_sw128(bb[gr] + kk * 2048, P, 1024), id2,
+                            (gr > 0 || kk > 0) ? 1u : 0u);
+        } else {
+            // O_i = L Y: A = L (M=j, K=k) K-major, B = Y (K=k, N=d) MN-major
+            const uint32_t id2 = idesc_bf16(128, 128, 0, 1);
+            const uint32_t aa[3] = {l_hi, l_hi, l_lo}, bb[3] = {y_hi, y_lo, y_hi};
+#pragma unroll
+            for (int gr = 0; gr < 3; ++gr)
+                for (uint32_t kk = 0; kk < nk; ++kk) {
+                    const uint32_t off = (kk >> 2) * P + (kk & 3) * 32;
+                    umma_ss(tmem, sdesc_sw128(aa[gr] + off, 16, 1024), sdesc_sw128(bb[gr] + kk * 2048, P, 1024), id2,
+                            (gr > 0 || kk > 0) ? 1u : 0u);
+                }
+        }
+        umma_commit(bar_mma2);
+    }
+    __syncwarp();
+
+    if (!FINAL && t < m) {
+        // cR[k,i] = sum_j L[j,k]  (monarch.hpp:139-143), k = t, from L hi + lo
+        float col[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const uint8_t* bh = smem + 4 * P + (t >> 6) * P;
+        const uint8_t* bl = smem + 6 * P + (t >> 6) * P;
+        auto lj = [&](int j) {
+            const uint32_t off = sw128_offset(j, t & 63);
+            return __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(bh + off)) +
+                   __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(bl + off));
+        };
+        int j = 0;
+        for (; j + 8 <= m; j += 8) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) col[e] += lj(j + e);
+        }
+        for (; j < m; ++j) col[0] += lj(j);
+        a.cR[((int64_t)u * m + t) * a.b + i] = ((col[0] + col[1]) + (col[2] + col[3])) + ((col[4] + col[5]) + (col[6] + col[7]));
+    }
+
+    // ---- epilogue: TMEM row t -> global (ITER: aR hi/lo bf16 rows (u, k=t, i); FINAL: O fp32
+    // row (u, token t*b + i))
+    mbar_wait(bar_mma2, 0);
+    tc_fence_after();
+    const bool store = t < m;
+    __nv_bfloat16* rh = nullptr;
+    __nv_bfloat16* rl = nullptr;
+    float* orow = nullptr;
+    if (!FINAL) {
+        const int64_t r = ((int64_t)u * m + t) * a.b + i;
+        rh = static_cast<__nv_bfloat16*>(a.ar_hi) + r * 128;
+        rl = static_cast<__nv_bfloat16*>(a.ar_lo) + r * 128;
+    } else {
+        orow = a.out + (int64_t)(u / a.oHn) * a.oB + (int64_t)(u % a.oHn) * a.oH + ((int64_t)t * a.b + i) * a.oT;
+    }
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+        uint32_t orr[32];
+        VMB_TMEM_LD32(tmem + lane_base + cc * 32, orr);
+        tmem_ld_wait();
+        if (!store) continue;
+        if (!FINAL) {
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+                uint4 h, l;
+                float f[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(orr[8 * x + e]) * a.qscale;
+                h.x = pack_bf16(f[0], f[1]);
+                h.y = pack_bf16(f[2], f[3]);
+                h.z = pack_bf16(f[4], f[5]);
+                h.w = pack_bf16(f[6], f[7]);
+                l.x = pack_bf16_residual(f[0], f[1], h.x);
+                l.y = pack_bf16_residual(f[2], f[3], h.y);
+                l.z = pack_bf16_residual(f[4], f[5], h.z);
+                l.w = pack_bf16_residual(f[6], f[7], h.w);
+                reinterpret_cast<uint4*>(rh + cc * 32)[x] = h;
+                reinterpret_cast<uint4*>(rl + cc * 32)[x] = l;
+            }
+        } else {
+#pragma unroll
+            for (int x = 0; x < 8; ++x)
+                reinterpret_cast<float4*>(orow + cc * 32)[x] =
+                    make_float4(__uint_as_float(orr[4 * x + 0]), __uint_as_float(orr[4 * x + 1]),
+                                __uint_as_float(orr[4 * x + 2]), __uint_as_float(orr[4 * x + 3]));
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc<128>(tmem);
+    }
+}
+
+template <bool FINAL, int NCH>
+void launch_hl_nch(const HlParams& p, int64_t U, cudaStream_t s) {
+    const HlLayout L(p.rows, FINAL);
+    const int smem = (int)L.bytes + 1024;
+    auto kern = lstep_hl_kernel<FINAL, NCH>;
+    VMB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    dim3 grid((unsigned)p.a.b, (unsigned)U);
+    ProfScope ps(FINAL ? kKLfinal : kKLstep, s);
+    kern<<<grid, kThreads, smem, s>>>(p);
+    count_launch();
+    check_launch("lstep_hl");
+}
+
+template <bool FINAL>
+void launch_hl(const HlParams& p, int64_t U, cudaStream_t s) {
+    switch ((p.rows + 31) / 32) {
+        case 1: launch_hl_nch<FINAL, 1>(p, U, s); break;
+        case 2: launch_hl_nch<FINAL, 2>(p, U, s); break;
+        case 3: launch_hl_nch<FINAL, 3>(p, U, s); break;
+        default: launch_hl_nch<FINAL, 4>(p, U, s); break;
+    }
+}
+
 template <bool FINAL, int NCH>
 void launch_nch(const Params& p, int64_t U, cudaStream_t s) {
     const Layout L(p.rows, FINAL);
@@ -315,6 +590,17 @@ void launch(const Params& p, int64_t U, cudaStream_t s) {
 }
 
 }  // namespace
+
+void tc_lstep_hl_launch(const TcLstepHlArgs& a, int64_t U, cudaStream_t s) {
+    if (U == 0 || a.b == 0) return;
+    VMB_REQUIRE_DIM(a.m >= 1 && a.m <= 128, "tcgen05 L-step requires m <= 128");
+    VMB_REQUIRE_DIM(a.b <= 2147483647 && U <= 65535, "tcgen05 L-step grid limits");
+    HlParams p;
+    p.a = a;
+    p.rows = lstep_rows(a.m);
+    if (a.final_mode) launch_hl<true>(p, U, s);
+    else launch_hl<false>(p, U, s);
+}
 
 void tc_lstep_launch(const TcLstepArgs& a, int64_t U, cudaStream_t s) {
     if (U == 0 || a.b == 0) return;

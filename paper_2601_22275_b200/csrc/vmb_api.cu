@@ -231,9 +231,10 @@ struct Workspace {
     float* part_o;    // split-KV partials of the first-frame recompute (tcgen05 path)
     float* part_lse;
     float* lse2;      // m > 128 (lstep_big.cu): row log-sum-exp of the L-step scores, (U, b, m)
-    // fp32 parity mode on tensor cores: hi/lo bf16 halves of Q, K, V and aR, (U, N, d) each
+    // fp32 parity mode on tensor cores: hi/lo bf16 halves of Q, K, V, (U, N, d) each (the
+    // state aR, aL, y is kept as hi/lo pairs in the halves of its fp32-sized buffer)
     void* qh = nullptr; void* ql = nullptr; void* kh = nullptr; void* kl = nullptr;
-    void* vh = nullptr; void* vl = nullptr; void* arh = nullptr; void* arl = nullptr;
+    void* vh = nullptr; void* vl = nullptr;
     int nsplit;
     size_t bytes;
 };
@@ -273,7 +274,7 @@ Workspace carve(void* base, const Shape& s, vmb_dtype dt) {
     w.nsplit = 1;
     if (dt == VMB_F32 && f32tc_shape(s)) {
         const size_t half = align_up((size_t)s.U * s.N * s.d * 2);
-        void** hl[8] = {&w.qh, &w.ql, &w.kh, &w.kl, &w.vh, &w.vl, &w.arh, &w.arl};
+        void** hl[6] = {&w.qh, &w.ql, &w.kh, &w.kl, &w.vh, &w.vl};
         for (void** x : hl) {
             *x = p + off;
             off += half;
@@ -404,7 +405,7 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
     const bool recompute = cfg.recompute_first_frame != 0;
     const bool skip_j0 = recompute && s.b == s.hw;
     const int64_t U = s.U, m = s.m, b = s.b, d = s.d, bq = s.bq;
-    VMB_CHECK_CUDA(cudaMemsetAsync(ws.status, 0, sizeof(int32_t), st));
+    VMB_CHECK_CUDA(cudaMemsetAsync(ws.status, 0, 2 * sizeof(int32_t), st));  // status, plan marker
     if (U == 0) return;
     const bool sharded = bq != b;
 
@@ -581,37 +582,55 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
     }
 
     // ---------------------------------------------------- fp32 parity mode on tensor cores
-    // Q, K, V (and each aR) are split into bf16 hi/lo halves; the R half-steps and the
-    // first-frame recompute run fa2's hilo instantiation (three bf16 MMA groups per product,
-    // fp32 accumulation and statistics, fp32 outputs); the L half-steps (HBM-light at fp32,
-    // ~1% of the FLOPs) run on the CUDA-core kernels.  The last R half-step computes aL and y
-    // in two passes over the same softmax (value = K, then V): fa2 holds one value operand.
+    // Q, K, V are split into bf16 hi/lo halves (x = hi + lo, 16 mantissa bits) and every
+    // product runs as three bf16 MMA groups with fp32 accumulation and statistics: the R
+    // half-steps and the first-frame recompute on fa2's hilo instantiation, the L half-steps
+    // on lstep_hl_kernel.  The half-step state aR, aL, y is carried as hi/lo pairs; O is fp32.
+    // The last R half-step computes aL and y in two passes over the same softmax rows (value
+    // = K, then V): fa2 holds one value operand.
     bool f32tc = dt == VMB_F32 && ws.qh != nullptr && aligned16(q) && aligned16(k) && aligned16(v) && aligned16(o);
     {
         const int64_t sts[6] = {in.batch, in.head, in.token, kin.batch, kin.head, kin.token};
         for (int64_t x : sts) f32tc = f32tc && x % 4 == 0;
+        f32tc = f32tc && out.token % 4 == 0 && out.head % 4 == 0 && out.batch % 4 == 0;
     }
     if (f32tc) {
+        // plan marker for vmb_export_factors: the state below is hi/lo pairs (status word + 4)
+        VMB_CHECK_CUDA(cudaMemsetAsync(reinterpret_cast<uint8_t*>(ws.status) + 4, 1, sizeof(int32_t), st));
         const int32_t Hm = (int32_t)std::max<int64_t>(s.H, 1);
-        const int64_t ud = m * b * d;
+        const size_t half = align_up((size_t)U * s.N * d * 2);
+        uint8_t* arh = static_cast<uint8_t*>(ws.aR);
+        uint8_t* alh = static_cast<uint8_t*>(ws.aL);
+        uint8_t* yh = static_cast<uint8_t*>(ws.y);
         split_hilo(user_view(q, in, s, 0, 1), U, s.N, d, ws.qh, ws.ql, st);
         split_hilo(user_view(k, kin, s, 0, 1), U, s.N, d, ws.kh, ws.kl, st);
         split_hilo(user_view(v, kin, s, 0, 1), U, s.N, d, ws.vh, ws.vl, st);
         const uint32_t bn = (uint32_t)tc2_kv_tile(1);
+        const uint32_t lrows = (uint32_t)lstep_rows(m);
         const CUtensorMap mQh = internal_map(ws.qh, U, m, b, d, true, 128, 1), mQl = internal_map(ws.ql, U, m, b, d, true, 128, 1);
         const CUtensorMap mKh = internal_map(ws.kh, U, m, b, d, true, bn, 1), mKl = internal_map(ws.kl, U, m, b, d, true, bn, 1);
         const CUtensorMap mVh = internal_map(ws.vh, U, m, b, d, true, bn, 1), mVl = internal_map(ws.vl, U, m, b, d, true, bn, 1);
-        const CUtensorMap mAh = internal_map(ws.arh, U, m, b, d, true, 128, 1), mAl = internal_map(ws.arl, U, m, b, d, true, 128, 1);
-        const View vQcol = user_view(q, in, s, 1, b);    // (u, i, j) -> token j*b+i
-        const View vAR = internal_view(ws.aR, ud, b * d, d);
-        const View vAL_in = internal_view(ws.aL, ud, m * d, d);
-        const View vY = internal_view(ws.y, ud, b * d, d);
-        const double qscale_d = 1.0 / std::sqrt((double)d);
+        const CUtensorMap mAh = internal_map(arh, U, m, b, d, true, 128, 1), mAl = internal_map(arh + half, U, m, b, d, true, 128, 1);
+        TcLstepHlArgs ls{};
+        ls.tmQ = internal_map(ws.qh, U, m, b, d, true, 1, lrows);      // Qb[i] boxes: (d, i, j)
+        ls.tmQlo = internal_map(ws.ql, U, m, b, d, true, 1, lrows);
+        ls.tmAL = internal_map(alh, U, b, m, d, true, lrows, 1);       // aL (U, b, m, d): (d, k, i)
+        ls.tmALlo = internal_map(alh + half, U, b, m, d, true, lrows, 1);
+        ls.tmY = internal_map(yh, U, m, b, d, true, 1, lrows);         // y (U, m, b, d): (d, i, k)
+        ls.tmYlo = internal_map(yh + half, U, m, b, d, true, 1, lrows);
+        ls.cL = ws.cL;
+        ls.qscale = qscale;
+        ls.m = (int32_t)m;
+        ls.b = (int32_t)b;
+        ls.cR = ws.cR;
+        ls.ar_hi = arh;
+        ls.ar_lo = arh + half;
+        ls.out = static_cast<float*>(o);
+        ls.oB = out.batch; ls.oH = out.head; ls.oT = out.token; ls.oHn = Hm;
         for (int64_t t = 0; t < cfg.iters; ++t) {
             const bool last = t == cfg.iters - 1;
             Tc2Args f2{};
             f2.hilo = 1;
-            f2.out_f32 = 1;
             f2.tmQ = t == 0 ? mQh : mAh;
             f2.tmQlo = t == 0 ? mQl : mAl;
             f2.tmK = f2.tmV = mKh;
@@ -622,7 +641,8 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
             f2.qscale = t == 0 ? qscale : 1.f;
             f2.clamp_min = (float)cfg.clamp_min; f2.clamp_enabled = cfg.clamp_enabled;
             f2.nv = 1;
-            f2.out = ws.aL;                       // aL (U, b, m, d) fp32: row (u, k, i)
+            f2.out = alh;                         // aL (U, b, m, d) hi/lo: row (u, k, i)
+            f2.out_lo = alh + half;
             f2.oB = b * m * d; f2.oH = 0; f2.oS = d; f2.oR = m * d;
             f2.cl_out = ws.cL;
             f2.status = ws.status;
@@ -634,27 +654,15 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
                 Tc2Args fy = f2;
                 fy.nv = 2;
                 fy.tmV = mVh; fy.tmVlo = mVl;
-                fy.out = ws.y;                    // y (U, m, b, d) fp32: row (u, k, i)
+                fy.out = yh;                      // y (U, m, b, d) hi/lo: row (u, k, i)
+                fy.out_lo = yh + half;
                 fy.oB = m * b * d; fy.oH = 0; fy.oS = b * d; fy.oR = d;
                 fy.cl_out = nullptr;
                 fy.check_finite = 0;
                 tc2_fa_launch(fy, U, st);
             }
-            SimtLstepArgs la{};
-            la.Q = vQcol;
-            la.qscale = qscale_d;
-            la.aL = vAL_in;
-            la.cL = ws.cL;
-            la.aR = vAR;
-            la.cR = ws.cR;
-            la.Y = vY;
-            la.O = user_view(o, out, s, b, 1);  // (u, j, i) -> token j*b+i
-            la.skip_j0 = skip_j0;
-            la.L = nullptr;
-            la.final_mode = last;
-            la.U = U; la.m = m; la.b = b; la.d = d;
-            simt_lstep(la, dt, st);
-            if (!last) split_hilo(internal_view(ws.aR, m * b * d, 0, d), U, m * b, d, ws.arh, ws.arl, st);
+            ls.final_mode = last;
+            tc_lstep_hl_launch(ls, U, st);
         }
         if (recompute) {
             // first-frame recompute (video.hpp:117-126): Q[0:hw) against all N keys, split over
@@ -1193,12 +1201,29 @@ vmb_status vmb_export_factors(const vmb_grid* grid, const vmb_config* cfg, vmb_d
         const Workspace ws = carve(workspace, s, dtype);
         cudaStream_t st = as_stream(stream);
         const int64_t m = s.m, b = s.b, d = s.d, ud = m * b * d;
+        // the fp32 tensor-core plan keeps aR / aL as bf16 hi/lo pairs: rebuild fp32 copies
+        int32_t hl_plan = 0;
+        if (dtype == VMB_F32 && ws.qh) {
+            VMB_CHECK_CUDA(cudaMemcpyAsync(&hl_plan, reinterpret_cast<const uint8_t*>(ws.status) + 4, sizeof(int32_t),
+                                           cudaMemcpyDeviceToHost, st));
+            VMB_CHECK_CUDA(cudaStreamSynchronize(st));
+        }
+        float* aR32 = static_cast<float*>(ws.aR);
+        float* aL32 = static_cast<float*>(ws.aL);
+        if (hl_plan) {
+            const int64_t n = s.U * s.N * d;
+            const size_t half = align_up((size_t)n * 2);
+            scratch_alloc(reinterpret_cast<void**>(&aR32), sizeof(float) * n, st);
+            scratch_alloc(reinterpret_cast<void**>(&aL32), sizeof(float) * n, st);
+            merge_hilo(ws.aR, static_cast<const uint8_t*>(ws.aR) + half, aR32, n, st);
+            merge_hilo(ws.aL, static_cast<const uint8_t*>(ws.aL) + half, aL32, n, st);
+        }
         if (R) {
             // R of the last R half-step, recomputed from that step's inputs, which the
             // workspace still holds (aR/cR of iteration iters-2, or Q itself when iters == 1).
             SimtRstepArgs ra{};
             const bool first = cfg->iters == 1;
-            ra.A = first ? user_view(q, *in, s, b, 1) : internal_view(ws.aR, ud, b * d, d);
+            ra.A = first ? user_view(q, *in, s, b, 1) : internal_view(aR32, ud, b * d, d);
             ra.qscale = first ? qscale : 1.0;
             ra.cR = first ? nullptr : ws.cR;
             ra.clamp_min = cfg->clamp_min;
@@ -1217,7 +1242,7 @@ vmb_status vmb_export_factors(const vmb_grid* grid, const vmb_config* cfg, vmb_d
             SimtLstepArgs la{};
             la.Q = user_view(q, *in, s, 1, b);
             la.qscale = qscale;
-            la.aL = internal_view(ws.aL, ud, m * d, d);
+            la.aL = internal_view(aL32, ud, m * d, d);
             la.cL = ws.cL;
             la.aR = internal_view(ws.aR, ud, b * d, d);
             la.cR = ws.cR;
@@ -1225,6 +1250,10 @@ vmb_status vmb_export_factors(const vmb_grid* grid, const vmb_config* cfg, vmb_d
             la.final_mode = 0;
             la.U = s.U; la.m = m; la.b = b; la.d = d;
             simt_lstep(la, dtype, st);
+        }
+        if (hl_plan) {
+            VMB_CHECK_CUDA(cudaFreeAsync(aR32, st));
+            VMB_CHECK_CUDA(cudaFreeAsync(aL32, st));
         }
     });
 }

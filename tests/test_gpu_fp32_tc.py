@@ -95,3 +95,27 @@ def test_fp32_c2_one_head(vm, orc, cuda):
     err = relfro(got, ref)
     print(f"fp32 tensor-core C2 one head: rel-Fro {err:.2e}")
     assert err <= F32_TOL
+
+
+def test_fp32_tensor_core_factor_export(vm, orc, cuda):
+    # MonarchFactors after the tensor-core plan: the export rebuilds fp32 aR / aL from their
+    # hi/lo pairs (vmb_export_factors), so L and R match the oracle's f32 factors
+    import ctypes as C
+    grid = vm.TokenGrid(3, 4, 10, 128, 1, 1)
+    cfg = vm.VMonarchConfig(iters=2, recompute_first_frame=False)
+    q, k, v = workload(1, grid.tokens(), 128, seed=21)
+    f = []
+    vm.vmonarch_attention(*(torch.from_numpy(x).to(cuda) for x in (q, k, v)), grid, cfg, factors_out=f)
+    L, R = (t.cpu().numpy() for t in f[0])
+    m, b = 3, 40
+    rL = np.zeros((b, m, m), np.float32)
+    rR = np.zeros((m, b, b), np.float32)
+    out = np.zeros((grid.tokens(), 128), np.float32)
+    fn = orc.lib.vmo_vmonarch_unit_f32
+    fn.argtypes = [C.c_void_p] * 3 + [C.c_int64] * 5 + [C.c_double, C.c_int, C.c_int] + [C.c_int64] * 4 + \
+        [C.c_void_p] * 3
+    ptr = lambda a: np.ascontiguousarray(a).ctypes.data_as(C.c_void_p)  # noqa: E731
+    qq, kk, vv = (np.ascontiguousarray(x[0]) for x in (q, k, v))
+    assert fn(ptr(qq), ptr(kk), ptr(vv), 3, 4, 10, 128, 2, 0.1, 1, 0, 0, 0, 64, 64, ptr(out), ptr(rL), ptr(rR)) == 0
+    assert np.abs(L - rL).max() <= 1e-4
+    assert np.abs(R - rR).max() <= 1e-4
