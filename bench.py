@@ -207,10 +207,14 @@ def main():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-chunk", type=int, default=2, help="heads per H2D/compute/D2H chunk in the e2e path")
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"],
+                    help="bf16 (the headline) or f32: the fp32 parity mode (tensor cores, hi/lo bf16 operands)")
     ap.add_argument("--shard", default="heads", choices=["heads", "seq"],
                     help="multi-GPU split: heads (no inter-GPU traffic) or seq (spatial slabs, NCCL K/V all-gather)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.dtype == "f32" and args.shard != "heads":
+        ap.error("--dtype f32 runs with --shard heads (the sequence-sharded mode is bf16)")
 
     if args.impl == "reference":
         run_reference_arm(args)
@@ -240,9 +244,10 @@ def main():
         grid = vm.TokenGrid(T, h, w, d, my_heads, 1)
         n = grid.tokens()
         nq_local = n
-        q = torch.randn((my_heads, n, d), device=dev, dtype=torch.bfloat16, generator=gen)
-        k = torch.randn((my_heads, n, d), device=dev, dtype=torch.bfloat16, generator=gen)
-        v = torch.randn((my_heads, n, d), device=dev, dtype=torch.bfloat16, generator=gen)
+        tdt = torch.float32 if args.dtype == "f32" else torch.bfloat16
+        q = torch.randn((my_heads, n, d), device=dev, dtype=tdt, generator=gen)
+        k = torch.randn((my_heads, n, d), device=dev, dtype=tdt, generator=gen)
+        v = torch.randn((my_heads, n, d), device=dev, dtype=tdt, generator=gen)
         o = torch.empty_like(q)
 
         def step(check=False):
@@ -333,6 +338,10 @@ def main():
     alg = kernel_algorithmic(grid, my_heads, nq_local / n)
     dom = max((k_ for k_ in kern if k_ in alg), key=lambda k_: kern[k_]["share"], default=None)
     roof = None
+    if args.dtype == "f32":
+        # the fp32 mode's kernels run three bf16 MMA groups per product and the y pass as a
+        # second launch, so the bf16 per-kernel algorithmic map does not apply
+        alg, dom = {}, None
     if dom:
         bound, work = alg[dom]
         t = kern[dom]["ms_per_launch"] * 1e-3
@@ -388,7 +397,7 @@ def main():
     # ---- dense bf16 attention on the same GPU and heads: our tcgen05 kernel (fa3, the same
     # kernel family as the recompute) and torch's SDPA (FlashAttention / cuDNN backends)
     dense = None
-    if not args.no_dense and args.shard == "heads" and args.config != "c5":
+    if not args.no_dense and args.shard == "heads" and args.config != "c5" and args.dtype == "bf16":
         dflops = 4.0 * n * n * d * my_heads
 
         def timed(fn, reps=3):
@@ -436,12 +445,12 @@ def main():
             got = o[:P].float().cpu().numpy()
             diff = got.astype(np.float64) - ref_out
             parity = {"units": P, "relfro": float(np.linalg.norm(diff) / np.linalg.norm(ref_out)),
-                      "max_abs": float(np.abs(diff).max()), "tolerance": 2e-2,
-                      "against": f"{info['kind']} CPU path (oracle/_ref) on the GPU arm's own bf16 inputs"}
+                      "max_abs": float(np.abs(diff).max()), "tolerance": 2e-2 if args.dtype == "bf16" else 1e-4,
+                      "against": f"{info['kind']} CPU path (oracle/_ref) on the GPU arm's own {args.dtype} inputs"}
             waves = -(-heads // P)
             cpu = {"value": round(sec * 1000.0 * waves, 1), "unit": "ms/call", "cores": info["threads"],
                    "kind": info["kind"],
-                   "sample": (f"{P} of the {heads} head units of {args.config.upper()} (the GPU arm's bf16 inputs), "
+                   "sample": (f"{P} of the {heads} head units of {args.config.upper()} (the GPU arm's {args.dtype} inputs), "
                               f"{info['threads']} threads, one unit each: {sec:.1f} s, scaled x{waves} waves to "
                               "ms/call (--impl reference measures a whole call)")}
         except Exception as ex:  # noqa
@@ -451,8 +460,8 @@ def main():
         line = {
             "metric": METRIC, "value": round(ms, 3), "unit": "ms/call", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "strong",
-            "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic N(0,1) bf16 Q/K/V (torch.Generator seed 1234+rank), resident in HBM",
+            "vs_baseline": None, "dtype": args.dtype,
+            "data": f"synthetic N(0,1) {args.dtype} Q/K/V (torch.Generator seed 1234+rank), resident in HBM",
             "config": {"workload": desc, "global_heads": heads, "heads_per_gpu": per, "seq_len": n,
                        "parallelism": (f"{args.shard}/{world}" if world > 1 else "single GPU"),
                        "l2": "inputs 1.2 GB per tensor (>126 MB L2); no flush needed"},
