@@ -174,6 +174,11 @@ struct Tc2Args {
     // optional low half of the bf16 output (R half-step: aL = hi + lo, hi = bf16(aL),
     // lo = bf16(aL - hi)), same layout as `out`; nullptr = not written
     void* out_lo;
+    // bf16 plan, aL's low half (§5 of DESIGN.md): aln_out receives |aL row| (layout as cl_out);
+    // qn_out (first R half-step) the max over frames of |Q row|^2 per (unit, position), (U, q_len)
+    // (atomicMax; zeroed by the caller)
+    float* aln_out;
+    float* qn_out;
     // fp32 parity mode on tensor cores (hilo = 1): every operand is a pair of bf16 tensors
     // x = hi + lo; tmQ/tmK/tmV map the hi halves, these the lo halves (same boxes).  Products
     // run as three bf16 MMA groups (hi hi + hi lo + lo hi) into fp32.  out_f32: `out` rows are
@@ -234,7 +239,14 @@ struct Tc4Args {
     int32_t qrHn;
     int32_t out_align32;         // every output row 32-byte aligned: 256-bit epilogue stores
     void* out0_lo;               // optional low half of operand 0 (aL), laid out as out0
-};
+    // the low half is written for a row only where the L-step can need it: qn == nullptr
+    // (always) or qn[u] * |aL row|^2 > lo_thresh2 (qn: max |Q row|^2 of the unit, from the first
+    // R half-step, per (unit, position): (U, q_len)); aln_out / qn_out as in Tc2Args
+    const float* qn;
+    float lo_thresh2;
+    float* aln_out;
+    float* qn_out;
+};  // (Tc4Args)
 int tc4_plan_splits(int64_t q_len, int64_t kv_len, int64_t n_useg, int max_split);
 void tc4_fa_launch(Tc4Args a, int64_t U, cudaStream_t s);
 // All L-step tiles are boxes of `rows = lstep_rows(m)` rows (m rounded up to 16); rows
@@ -253,16 +265,20 @@ struct TcLstepArgs {
     int32_t final_mode;
     float* cR;          // ITER: (U, m, b)
     float out_scale;    // multiplies the epilogue (ITER: aR scale)
-    // aL = hi + lo (the R half-step writes both halves): the low half, same boxes as tmAL.
-    // It is read only by CTAs whose score tile exceeds kLstepLoGate (use_lo = 0: never).
+    // aL = hi + lo (the R half-step writes the low half where it can matter): the low half,
+    // same boxes as tmAL (use_lo = 0: never read).  The logit error of the hi half alone for
+    // row k is at most qscale |Qb_j| |aL_k - hi_k| <= qscale Qmax |aL_k| 2^-9, so row k uses
+    // its low half iff qscale^2 Qmax^2 |aL_k|^2 > kLoBound^2, i.e. qn[u, i] aln[k]^2 > lo_thresh2
+    // (aln: (U, b, m) row norms of aL from the R half-step; qn: (U, b) max over the block's
+    // query rows Qb[i][j] of |Q row|^2).
     CUtensorMap tmALlo;
     int32_t use_lo;
+    const float* aln;
+    const float* qn;
+    float lo_thresh2;
 };
-// The L-step adds the low half of aL to its scores only where bf16 aL could move a logit:
-// the rounding error of <Qb_j, aL_k> grows with |Qb_j| |aL_k|, and max |S| over the tile
-// tracks that product.  Below this max |S| (natural-log logits) the hi half alone keeps the
-// logit error under ~1e-3.
-constexpr float kLstepLoGate = 2.0f;
+// Logit-error bound below which a row of aL needs no low half: 2 * 2^-9 ~ 3.9e-3.
+constexpr float kLoBound = 2.0f;
 void tc_lstep_launch(const TcLstepArgs& a, int64_t U, cudaStream_t s);
 // The fp32 parity mode's L half-step / apply on tensor cores (lstep_tc.cu, lstep_hl_kernel):
 // every operand is a bf16 hi/lo pair (x = hi + lo), each product three bf16 MMA groups into

@@ -296,6 +296,28 @@ __global__ void __launch_bounds__(kThreads, HL ? 1 : 2) fa2_kernel(const __grid_
                 }
             }
             if (bad && valid) atomicExch(a.status, kStatusNonFiniteQ);
+            if (a.qn_out) {
+                // max |Q row|^2 of the unit (bounds the L-step logits; nonnegative floats order as ints)
+                float ss = 0.f;
+#pragma unroll
+                for (int pnl = 0; pnl < 2; ++pnl) {
+                    const uint4* q4 = reinterpret_cast<const uint4*>(smem + SM::q_off + pnl * kQPanel + row * 128);
+#pragma unroll
+                    for (int x = 0; x < 8; ++x) {
+                        const uint4 v = q4[x ^ (row & 7)];
+                        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float lo = __uint_as_float(w[e] << 16), hi = __uint_as_float(w[e] & 0xFFFF0000u);
+                            ss = fmaf(lo, lo, fmaf(hi, hi, ss));
+                        }
+                    }
+                }
+                // per spatial position i = row: the max over frames of |Q row|^2 (nonnegative floats
+                // order as ints); the L-step block of position i has exactly these rows as queries
+                if (valid && !bad)
+                    atomicMax(reinterpret_cast<unsigned*>(a.qn_out) + (int64_t)u * a.q_len + grow, __float_as_uint(ss));
+            }
         }
 
         float m_run = -INFINITY, l_run = 0.f;
@@ -440,6 +462,7 @@ __global__ void __launch_bounds__(kThreads, HL ? 1 : 2) fa2_kernel(const __grid_
             const int64_t ob = u / a.oHn, oh = u % a.oHn;
             __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(a.out) + ob * a.oB + oh * a.oH + (int64_t)seg * a.oS +
                                   (int64_t)grow * a.oR;
+            float ssa = 0.f;  // |output row|^2 (aln_out)
 #pragma unroll
             for (int cc = 0; cc < 4; ++cc) {
                 uint32_t orr[32];
@@ -488,7 +511,10 @@ __global__ void __launch_bounds__(kThreads, HL ? 1 : 2) fa2_kernel(const __grid_
                 } else if (valid) {
                     float f[32];
 #pragma unroll
-                    for (int x = 0; x < 32; ++x) f[x] = __uint_as_float(orr[x]) * inv_l;
+                    for (int x = 0; x < 32; ++x) {
+                        f[x] = __uint_as_float(orr[x]) * inv_l;
+                        ssa = fmaf(f[x], f[x], ssa);
+                    }
                     uint4 v[4];
 #pragma unroll
                     for (int x = 0; x < 4; ++x) {
@@ -529,6 +555,7 @@ __global__ void __launch_bounds__(kThreads, HL ? 1 : 2) fa2_kernel(const __grid_
             if (valid) {
                 if (a.cl_out)
                     a.cl_out[((int64_t)u * a.q_len + grow) * a.nseg + seg] = kLn2 * (scale2 * qo * inv_l - lse2);
+                if (a.aln_out) a.aln_out[((int64_t)u * a.q_len + grow) * a.nseg + seg] = sqrtf(ssa);
                 if (a.lse_out) a.lse_out[((int64_t)u * a.nseg + seg) * a.q_len + grow] = kLn2 * lse2;
             }
         }

@@ -359,6 +359,26 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                     }
                 }
                 if (bad && valid) atomicExch(a.status, kStatusNonFiniteQ);
+                if (a.qn_out) {
+                    // max |Q row|^2 of the unit (bounds the L-step logits; nonnegative floats order as ints)
+                    float ss = 0.f;
+#pragma unroll
+                    for (int pnl = 0; pnl < 2; ++pnl) {
+                        const uint4* q4 = reinterpret_cast<const uint4*>(qsm + pnl * kPanel + row * 128);
+#pragma unroll
+                        for (int x = 0; x < 8; ++x) {
+                            const uint4 v = q4[x ^ (row & 7)];
+                            const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const float lo = __uint_as_float(wd[e] << 16), hi = __uint_as_float(wd[e] & 0xFFFF0000u);
+                                ss = fmaf(lo, lo, fmaf(hi, hi, ss));
+                            }
+                        }
+                    }
+                    if (valid && !bad)
+                        atomicMax(reinterpret_cast<unsigned*>(a.qn_out) + (int64_t)w.u * a.q_len + grow, __float_as_uint(ss));
+                }
             }
 
             float m_run = -INFINITY, l_run = 0.f;
@@ -522,7 +542,8 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                 mbar_arrive(&o_empty[ob]);
                 if (valid) a.part_lse[((int64_t)w.useg * a.nsplit + w.split) * a.q_len + grow] = kLn2 * lse2;
             } else {
-                float qo = 0.f;  // <q_row, (P K)_row> (R-step entropy)
+                float qo = 0.f;   // <q_row, (P K)_row> (R-step entropy)
+                float ssa = 0.f;  // |aL row|^2: decides its low half and feeds aln_out
                 const int64_t obh = w.u / a.oHn, ohh = w.u % a.oHn;
 #pragma unroll
                 for (int t = 0; t < NO; ++t) {
@@ -554,7 +575,10 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                         if (valid) {
                             float f[32];
 #pragma unroll
-                            for (int x = 0; x < 32; ++x) f[x] = __uint_as_float(orr[x]) * inv_l;
+                            for (int x = 0; x < 32; ++x) {
+                                f[x] = __uint_as_float(orr[x]) * inv_l;
+                                if (t == 0) ssa = fmaf(f[x], f[x], ssa);
+                            }
                             uint4 v[4];
 #pragma unroll
                             for (int x = 0; x < 4; ++x) {
@@ -575,10 +599,18 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                             }
                         }
                     }
-                    if (t == 0 && a.out0_lo) {
-                        // low half of aL (same layout): bf16(x - bf16(x)), a second TMEM pass so
-                        // the entropy dot's prefetched q row is dead by then (register budget).
-                        // tcgen05.ld is warp-collective: every lane loads, only valid rows store.
+                    // low half of aL (same layout): bf16(x - bf16(x)), only for rows whose L-step
+                    // logits could move by more than the bound (qn: Qmax^2 of the unit; nullptr:
+                    // not known yet -> every row), a second TMEM pass so the entropy dot's
+                    // prefetched q row is dead by then (register budget).  tcgen05.ld is
+                    // warp-collective: a warp with any such row loads, only those rows store.
+                    const bool need_lo =
+                        valid && (a.qn == nullptr || a.qn[(int64_t)w.u * a.q_len + grow] * ssa > a.lo_thresh2);
+                    if (t == 0 && a.out0_lo && NO == 1 && !__any_sync(0xffffffffu, need_lo)) {
+                        tc_fence_before();
+                        mbar_arrive(&o_empty[ob]);
+                    }
+                    if (t == 0 && a.out0_lo && __any_sync(0xffffffffu, need_lo)) {
                         __nv_bfloat16* lrow = static_cast<__nv_bfloat16*>(a.out0_lo) + obh * a.oB[0] + ohh * a.oH[0] +
                                               (int64_t)w.seg * a.oS[0] + (int64_t)grow * a.oR[0];
 #pragma unroll 1
@@ -590,7 +622,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                                 tc_fence_before();
                                 mbar_arrive(&o_empty[ob]);
                             }
-                            if (valid) {
+                            if (need_lo) {
                                 uint4 v[4];
 #pragma unroll
                                 for (int x = 0; x < 4; ++x) {
@@ -621,6 +653,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                 if (valid) {
                     if (a.cl_out)
                         a.cl_out[((int64_t)w.u * a.q_len + grow) * a.nseg + w.seg] = kLn2 * (scale2 * qo * inv_l - lse2);
+                    if (a.aln_out) a.aln_out[((int64_t)w.u * a.q_len + grow) * a.nseg + w.seg] = sqrtf(ssa);
                     if (a.lse_out) a.lse_out[((int64_t)w.u * a.nseg + w.seg) * a.q_len + grow] = kLn2 * lse2;
                 }
                 if (threadIdx.x == 192) TRACE4(n, 6);

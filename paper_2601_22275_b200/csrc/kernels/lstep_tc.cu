@@ -111,8 +111,12 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
     // cL[i, 0..m) -> smem (all rows of this block share it)
     const float* cl = a.cL + ((int64_t)u * a.b + i) * m;
     if (t < R) s_cl[t] = (t < m) ? cl[t] : 0.f;
+    // row k = t of aL needs its low half iff the hi half alone could move an L-step logit by more
+    // than kLoBound * 2^-9: qscale Qmax |aL_k| > kLoBound (Cauchy-Schwarz over the block's queries)
+    const bool need_lo = a.use_lo && t < m && a.qn[(int64_t)u * a.b + i] * (a.aln[((int64_t)u * a.b + i) * m + t] *
+                                                                          a.aln[((int64_t)u * a.b + i) * m + t]) > a.lo_thresh2;
     tc_fence_before();
-    __syncthreads();
+    const int any_lo = __syncthreads_or(need_lo);
     tc_fence_after();
     const uint32_t tmem = *slot;
     const bool leader = (warp == 0) && elect_one();
@@ -134,44 +138,44 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
     mbar_wait(bar_mma1, 0);
     tc_fence_after();
     uint32_t sr[NCH * 32];
+    if (any_lo) {
+        // aL = hi + lo: S += Qb aL_lo^T for the rows that need it.  GEMM 1 has finished reading
+        // aL hi (bar_mma1): the low half lands in its place; rows whose low half the R half-step
+        // did not write (or does not matter) are zeroed before the MMA reads the tile.
+        if (leader) {
+            mbar_arrive_expect_tx(bar_lo, 2u * L.panel);
+            tma_load_5d(smem + L.al, &a.tmALlo, bar_lo, 0, 0, i, 0, u);
+            tma_load_5d(smem + L.al + L.panel, &a.tmALlo, bar_lo, 64, 0, i, 0, u);
+        }
+        __syncwarp();
+        mbar_wait(bar_lo, 0);
+        if (t < R && !need_lo) {
+            uint4* r0 = reinterpret_cast<uint4*>(smem + L.al + t * 128);
+            uint4* r1 = reinterpret_cast<uint4*>(smem + L.al + L.panel + t * 128);
+#pragma unroll
+            for (int x = 0; x < 8; ++x) r0[x] = r1[x] = make_uint4(0, 0, 0, 0);
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+        if (leader) {
+            const uint32_t id1 = idesc_bf16(128, (uint32_t)R, 0, 0);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                const uint32_t off = (kk >> 2) * L.panel + (kk & 3) * 32;
+                umma_ss(tmem, sdesc_sw128(qb_addr + off, 16, 1024), sdesc_sw128(al_addr + off, 16, 1024), id1, 1u);
+            }
+            umma_commit(bar_mma1b);
+        }
+        __syncwarp();
+        mbar_wait(bar_mma1b, 0);
+        tc_fence_after();
+    }
 #pragma unroll
     for (int c = 0; c < NCH; ++c) VMB_TMEM_LD32(tmem + lane_base + c * 32, (sr + c * 32));
     tmem_ld_wait();
     float* s = reinterpret_cast<float*>(sr);
-    if (a.use_lo) {
-        // aL = hi + lo: add Qb aL_lo^T where the hi half alone could move a logit (kLstepLoGate)
-        float amax = 0.f;
-#pragma unroll
-        for (int k = 0; k < NCH * 32; ++k) amax = (k < m) ? fmaxf(amax, fabsf(s[k])) : amax;
-        // TMEM lanes t >= m hold don't-care rows (the M = 128 MMA reads past Qb's R rows into
-        // whatever shared memory follows): they must not steer the gate
-        if (t >= m) amax = 0.f;
-        tc_fence_before();
-        if (__syncthreads_or(amax * a.qscale > kLstepLoGate)) {
-            if (leader) {
-                // GEMM 1 has finished reading aL_hi (bar_mma1): the low half lands in its place
-                mbar_arrive_expect_tx(bar_lo, 2u * L.panel);
-                tma_load_5d(smem + L.al, &a.tmALlo, bar_lo, 0, 0, i, 0, u);
-                tma_load_5d(smem + L.al + L.panel, &a.tmALlo, bar_lo, 64, 0, i, 0, u);
-                mbar_wait(bar_lo, 0);
-                tc_fence_after();
-                const uint32_t id1 = idesc_bf16(128, (uint32_t)R, 0, 0);
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint32_t off = (kk >> 2) * L.panel + (kk & 3) * 32;
-                    umma_ss(tmem, sdesc_sw128(qb_addr + off, 16, 1024), sdesc_sw128(al_addr + off, 16, 1024), id1, 1u);
-                }
-                umma_commit(bar_mma1b);
-            }
-            __syncwarp();
-            mbar_wait(bar_mma1b, 0);
-            tc_fence_after();
-#pragma unroll
-            for (int c = 0; c < NCH; ++c) VMB_TMEM_LD32(tmem + lane_base + c * 32, (sr + c * 32));
-            tmem_ld_wait();
-        }
-        tc_fence_after();
-    }
     const float sc2 = a.qscale * kLog2e;
     float mx = -INFINITY;
 #pragma unroll

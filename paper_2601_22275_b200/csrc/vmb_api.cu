@@ -218,6 +218,9 @@ Shape make_shape(const vmb_grid* g, const vmb_config* c) {
     return s;
 }
 
+#ifndef VMB_EXP_NO_LO  // experiment builds only: no low half of aL (round-1 precision)
+#define VMB_EXP_NO_LO 0
+#endif
 size_t dtype_bytes(vmb_dtype dt) { return dt == VMB_BF16 ? 2 : dt == VMB_F64 ? 8 : 4; }
 
 struct Workspace {
@@ -226,6 +229,8 @@ struct Workspace {
     void* aL;
     void* y;
     void* aL_lo;      // low half of aL (bf16 tcgen05 path, m <= 128): aL = aL + aL_lo
+    float* aln;       // |aL row| (U, b, m), written by the R half-steps (bf16 tcgen05 path)
+    float* qn;        // (U, b): max over frames of |Q row|^2 per spatial position (first R half-step)
     float* cR;
     float* cL;
     float* part_o;    // split-KV partials of the first-frame recompute (tcgen05 path)
@@ -259,9 +264,14 @@ Workspace carve(void* base, const Shape& s, vmb_dtype dt) {
     w.aL = p + off; off += act;
     w.y = p + off; off += act;
     w.aL_lo = nullptr;
-    if (dt == VMB_BF16 && s.d == 128 && s.m <= 128) {
+    w.aln = w.qn = nullptr;
+    if (dt == VMB_BF16 && s.d == 128 && s.m <= 128 && !VMB_EXP_NO_LO) {
         w.aL_lo = p + off;
         off += act;
+        w.aln = reinterpret_cast<float*>(p + off);
+        off += align_up((size_t)s.U * s.Nq * sizeof(float));
+        w.qn = reinterpret_cast<float*>(p + off);
+        off += align_up((size_t)s.U * s.bq * sizeof(float));
     }
     w.cR = reinterpret_cast<float*>(p + off); off += st;
     w.cL = reinterpret_cast<float*>(p + off); off += st;
@@ -412,6 +422,12 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
     if (tc_eligible(s, dt, in, out, q, k, v, o) && tc_eligible(s, dt, kin, out, q, k, v, o)) {
         // ------------------------------------------------ tcgen05 path
         const int32_t Hm = (int32_t)std::max<int64_t>(s.H, 1);
+        // aL's low half is kept where the L-step logits need it: qscale Qmax |aL_k| > kLoBound
+        // (lstep_tc.cu), Qmax per spatial position from the first R half-step's Q tiles (a
+        // position's bound involves only its own rows: the result does not depend on how units
+        // or positions are sharded)
+        if (ws.qn) VMB_CHECK_CUDA(cudaMemsetAsync(ws.qn, 0, sizeof(float) * U * bq, st));
+        const float lo_thresh2 = kLoBound * kLoBound / (qscale * qscale);
         const CUtensorMap mQrow = user_map(q, in, s, bq, 1, m, bq, 128, 1);    // (d, i, k): query tiles
         const CUtensorMap mK = user_map(k, kin, s, b, 1, m, b, 128, 1);        // fa4: 128-key tiles
         const CUtensorMap mV = user_map(v, kin, s, b, 1, m, b, 128, 1);
@@ -448,6 +464,10 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
                 f4.oB[1] = m * bq * d; f4.oH[1] = 0; f4.oS[1] = bq * d; f4.oR[1] = d;
                 f4.cl_out = ws.cL;
                 f4.out0_lo = ws.aL_lo;
+                f4.aln_out = ws.aln;
+                f4.qn = t == 0 ? nullptr : ws.qn;       // t = 0: Qmax not known yet, every row
+                f4.qn_out = t == 0 ? ws.qn : nullptr;
+                f4.lo_thresh2 = lo_thresh2;
                 f4.status = ws.status;
                 f4.check_finite = t == 0;
                 f4.max_split = 1;
@@ -471,6 +491,10 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
                 f4.oB[0] = bq * m * d; f4.oH[0] = 0; f4.oS[0] = d; f4.oR[0] = m * d;
                 f4.cl_out = ws.cL;
                 f4.out0_lo = ws.aL_lo;
+                f4.aln_out = ws.aln;
+                f4.qn = t == 0 ? nullptr : ws.qn;
+                f4.qn_out = t == 0 ? ws.qn : nullptr;
+                f4.lo_thresh2 = lo_thresh2;
                 f4.status = ws.status;
                 f4.check_finite = t == 0;
                 f4.max_split = 1;
@@ -493,7 +517,9 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
                 f2.out = ws.aL;
                 f2.oB = bq * m * d; f2.oH = 0; f2.oS = d; f2.oR = m * d;
                 f2.cl_out = ws.cL;
-                f2.out_lo = ws.aL_lo;
+                f2.out_lo = ws.aL_lo;                 // every row: fa2 runs before Qmax is known (t = 0)
+                f2.aln_out = ws.aln;
+                f2.qn_out = t == 0 ? ws.qn : nullptr;
                 f2.status = ws.status;
                 f2.check_finite = t == 0;
                 f2.max_split = 1;
@@ -540,6 +566,9 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
                 ls.out_scale = last ? 1.f : qscale;
                 ls.tmALlo = mALlo;
                 ls.use_lo = ws.aL_lo != nullptr;
+                ls.aln = ws.aln;
+                ls.qn = ws.qn;
+                ls.lo_thresh2 = lo_thresh2;
                 tc_lstep_launch(ls, U, st);
             }
         }

@@ -22,7 +22,10 @@ OUT = os.path.join(HERE, "gpurun_out")
 PROF = os.path.join(HERE, "profiles")
 
 # kernel-name fragment -> bench.py kernel key
-KEYS = [("fa_tc_kernel<2, 2", "rstep_y"), ("fa_tc_kernel<1, 1", "rstep"), ("fa2_kernel<1>", "rstep"),
+KEYS = [("fa2_kernel<1, 1>", "rstep_f32"), ("fa2_kernel<2, 1>", "attn_f32"), ("fa2_kernel<1, 0>", "rstep"),
+        ("fa2_kernel<2, 0>", "attn_recompute"), ("lstep_hl_kernel<0", "lstep_f32"),
+        ("lstep_hl_kernel<1", "lstep_apply_f32"), ("split_hilo", "split_hilo"),
+        ("fa_tc_kernel<2, 2", "rstep_y"), ("fa_tc_kernel<1, 1", "rstep"), ("fa2_kernel<1>", "rstep"),
         ("fa2_kernel<2>", "attn_recompute"), ("fa3_kernel<2", "attn_recompute"), ("fa3_kernel<1", "rstep"),
         ("fa4_kernel<1, 1>", "rstep"), ("fa4_kernel<2, 2>", "rstep_y"), ("fa4_kernel<2, 1>", "attn_recompute"),
         ("fa6_kernel<2", "attn_recompute"), ("fa6_kernel<1", "rstep"),
