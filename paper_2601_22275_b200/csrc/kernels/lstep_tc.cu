@@ -79,6 +79,15 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
     const uint32_t qb_addr = smem_u32(smem + L.qb);
     const uint32_t al_addr = smem_u32(smem + L.al);
     const uint32_t y_addr = smem_u32(smem + L.y);
+    // the per-position scalars first: their global-load latency overlaps the barrier setup,
+    // the TMA issue and the TMEM allocation below
+    const int64_t pos = (int64_t)u * a.b + i;
+    const float clv = (t < m) ? __ldg(a.cL + pos * m + t) : 0.f;
+    float qnv = 0.f, alnv = 0.f;
+    if (a.use_lo && t < m) {
+        qnv = __ldg(a.qn + pos);
+        alnv = __ldg(a.aln + pos * m + t);
+    }
 
     if (warp == 0) {
         if (elect_one()) {
@@ -93,7 +102,7 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
             mbar_init(bar_lo, 1);
             mbar_init(bar_mma1b, 1);
             fence_mbar_init();
-            // loads first: their latency overlaps the TMEM allocation and the cL fetch
+            // loads first: their latency overlaps the TMEM allocation
             const int qbb = u / a.H, qh = u % a.H;
             mbar_arrive_expect_tx(bar_load, (FINAL ? 6u : 4u) * L.panel);
             tma_load_5d(smem + L.qb, &a.tmQ, bar_load, 0, i, 0, qh, qbb);
@@ -108,13 +117,12 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
         __syncwarp();
         tmem_alloc<128>(slot);
     }
-    // cL[i, 0..m) -> smem (all rows of this block share it)
-    const float* cl = a.cL + ((int64_t)u * a.b + i) * m;
-    if (t < R) s_cl[t] = (t < m) ? cl[t] : 0.f;
+    // cL[i, k] * log2(e) -> smem (all rows of this block share it); columns k >= m get +inf,
+    // so their logits are -inf and their exponentials 0 with no per-element select
+    s_cl[t] = (t < m) ? clv * kLog2e : INFINITY;
     // row k = t of aL needs its low half iff the hi half alone could move an L-step logit by more
     // than kLoBound * 2^-9: qscale Qmax |aL_k| > kLoBound (Cauchy-Schwarz over the block's queries)
-    const bool need_lo = a.use_lo && t < m && a.qn[(int64_t)u * a.b + i] * (a.aln[((int64_t)u * a.b + i) * m + t] *
-                                                                          a.aln[((int64_t)u * a.b + i) * m + t]) > a.lo_thresh2;
+    const bool need_lo = a.use_lo && t < m && qnv * (alnv * alnv) > a.lo_thresh2;
     tc_fence_before();
     const int any_lo = __syncthreads_or(need_lo);
     tc_fence_after();
@@ -172,37 +180,53 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
         mbar_wait(bar_mma1b, 0);
         tc_fence_after();
     }
+    if (warp * 32 < R) {  // (a warp past the R rows holds no row of L)
 #pragma unroll
-    for (int c = 0; c < NCH; ++c) VMB_TMEM_LD32(tmem + lane_base + c * 32, (sr + c * 32));
-    tmem_ld_wait();
-    float* s = reinterpret_cast<float*>(sr);
-    const float sc2 = a.qscale * kLog2e;
-    float mx = -INFINITY;
+        for (int c = 0; c < NCH; ++c) VMB_TMEM_LD32(tmem + lane_base + c * 32, (sr + c * 32));
+        tmem_ld_wait();
+        float* s = reinterpret_cast<float*>(sr);
+        // R = NCH*32 - 16: TMEM columns [R, NCH*32) are not written by GEMM 1 (don't-care data)
+        if (R < NCH * 32) {
 #pragma unroll
-    for (int k = 0; k < NCH * 32; ++k) {
-        s[k] = (k < m) ? (s[k] * sc2 - s_cl[k] * kLog2e) : -INFINITY;
-        mx = fmaxf(mx, s[k]);
-    }
-    float sum = 0.f;
+            for (int k = NCH * 32 - 16; k < NCH * 32; ++k) s[k] = 0.f;
+        }
+        const float sc2 = a.qscale * kLog2e;
+        const float4* c4 = reinterpret_cast<const float4*>(s_cl);
+        // base-2 logits x' = S * qscale * log2e - cL * log2e (k >= m: -inf); four independent
+        // max / sum chains
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-    for (int k = 0; k < NCH * 32; ++k) {
-        s[k] = (k < m) ? ex2(s[k] - mx) : 0.f;
-        sum += s[k];
-    }
-    // rows j >= m are written as zeros: they are part of GEMM 2's K extent (ITER)
-    const float inv = (t < m) ? 1.f / sum : 0.f;
-    // L row j -> bf16, SW128, over the consumed aL tile
-    if (t < R) {
-        uint8_t* lt = smem + L.al;
+        for (int k4 = 0; k4 < NCH * 8; ++k4) {
+            const float4 c = c4[k4];
+            s[4 * k4 + 0] = fmaf(s[4 * k4 + 0], sc2, -c.x);
+            s[4 * k4 + 1] = fmaf(s[4 * k4 + 1], sc2, -c.y);
+            s[4 * k4 + 2] = fmaf(s[4 * k4 + 2], sc2, -c.z);
+            s[4 * k4 + 3] = fmaf(s[4 * k4 + 3], sc2, -c.w);
 #pragma unroll
-        for (int c8 = 0; c8 < NCH * 4; ++c8) {
-            if (c8 * 8 < R) {
-                uint4 v;
-                v.x = pack_bf16(s[8 * c8 + 0] * inv, s[8 * c8 + 1] * inv);
-                v.y = pack_bf16(s[8 * c8 + 2] * inv, s[8 * c8 + 3] * inv);
-                v.z = pack_bf16(s[8 * c8 + 4] * inv, s[8 * c8 + 5] * inv);
-                v.w = pack_bf16(s[8 * c8 + 6] * inv, s[8 * c8 + 7] * inv);
-                *reinterpret_cast<uint4*>(lt + (c8 >> 3) * L.panel + sw128_offset(t, (c8 & 7) * 8)) = v;
+            for (int e = 0; e < 4; ++e) m4[e] = fmaxf(m4[e], s[4 * k4 + e]);
+        }
+        const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+        float s4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int k = 0; k < NCH * 32; ++k) {
+            s[k] = ex2(s[k] - mx);
+            s4[k & 3] += s[k];
+        }
+        // rows j >= m are written as zeros: they are part of GEMM 2's K extent (ITER)
+        const float inv = (t < m) ? 1.f / ((s4[0] + s4[1]) + (s4[2] + s4[3])) : 0.f;
+        // L row j -> bf16, SW128, over the consumed aL tile
+        if (t < R) {
+            uint8_t* lt = smem + L.al;
+#pragma unroll
+            for (int c8 = 0; c8 < NCH * 4; ++c8) {
+                if (c8 * 8 < R) {
+                    uint4 v;
+                    v.x = pack_bf16(s[8 * c8 + 0] * inv, s[8 * c8 + 1] * inv);
+                    v.y = pack_bf16(s[8 * c8 + 2] * inv, s[8 * c8 + 3] * inv);
+                    v.z = pack_bf16(s[8 * c8 + 4] * inv, s[8 * c8 + 5] * inv);
+                    v.w = pack_bf16(s[8 * c8 + 6] * inv, s[8 * c8 + 7] * inv);
+                    *reinterpret_cast<uint4*>(lt + (c8 >> 3) * L.panel + sw128_offset(t, (c8 & 7) * 8)) = v;
+                }
             }
         }
     }
@@ -232,22 +256,44 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
     }
     __syncwarp();
 
-    if (!FINAL && t < m) {
-        // cR[k,i] = sum_j L[j,k]  (monarch.hpp:139-143), k = t, from the bf16 copy of L
-        // 8 independent chains: the loads of a group issue back to back instead of one
-        // shared-memory latency per row
-        float col[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        const uint8_t* base = smem + L.al + (t >> 6) * L.panel;
-        auto lj = [&](int j) {
-            return __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(base + sw128_offset(j, t & 63)));
-        };
-        int j = 0;
-        for (; j + 8 <= m; j += 8) {
+    if (!FINAL) {
+        // cR[k,i] = sum_j L[j,k]  (monarch.hpp:139-143) from the bf16 copy of L, while GEMM 2
+        // runs: thread t sums the column pair (2p, 2p+1), p = t % 64, over half the rows (t < 64:
+        // j < mh, else j >= mh); 32-bit loads, four independent chains per column
+        const int p = t & 63, half = t >> 6;
+        const int mh = (m + 1) >> 1;
+        const int j0 = half ? mh : 0, j1 = half ? m : mh;
+        float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
+        if (2 * p < m) {
+            const uint8_t* base = smem + L.al + (p >> 5) * L.panel;
+            const uint32_t col = (2 * p) & 63;
+            int j = j0;
+            for (; j + 4 <= j1; j += 4) {
 #pragma unroll
-            for (int e = 0; e < 8; ++e) col[e] += lj(j + e);
+                for (int e = 0; e < 4; ++e) {
+                    const uint32_t w = *reinterpret_cast<const uint32_t*>(base + sw128_offset(j + e, col));
+                    c0[e] += __uint_as_float(w << 16);
+                    c1[e] += __uint_as_float(w & 0xFFFF0000u);
+                }
+            }
+            for (; j < j1; ++j) {
+                const uint32_t w = *reinterpret_cast<const uint32_t*>(base + sw128_offset(j, col));
+                c0[0] += __uint_as_float(w << 16);
+                c1[0] += __uint_as_float(w & 0xFFFF0000u);
+            }
         }
-        for (; j < m; ++j) col[0] += lj(j);  // (static index: col[] stays in registers)
-        a.cR[((int64_t)u * m + t) * a.b + i] = ((col[0] + col[1]) + (col[2] + col[3])) + ((col[4] + col[5]) + (col[6] + col[7]));
+        const float cs0 = (c0[0] + c0[1]) + (c0[2] + c0[3]);
+        const float cs1 = (c1[0] + c1[1]) + (c1[2] + c1[3]);
+        // the upper half hands its partial sums over through the (consumed) cL slots
+        float2* part = reinterpret_cast<float2*>(s_cl);
+        if (half) part[p] = make_float2(cs0, cs1);
+        __syncthreads();
+        if (!half && 2 * p < m) {
+            const float2 q = part[p];
+            float* cr = a.cR + ((int64_t)u * m + 2 * p) * a.b + i;
+            cr[0] = cs0 + q.x;
+            if (2 * p + 1 < m) cr[a.b] = cs1 + q.y;
+        }
     }
 
     // ---- epilogue: TMEM row t -> bf16 SW128 staging tile over Qb -> TMA store
@@ -256,6 +302,7 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
     const float scale = a.out_scale;
 #pragma unroll
     for (int cc = 0; cc < 4; ++cc) {
+        if (warp * 32 >= R) break;  // no output row in this warp
         uint32_t orr[32];
         VMB_TMEM_LD32(tmem + lane_base + cc * 32, orr);
         tmem_ld_wait();
