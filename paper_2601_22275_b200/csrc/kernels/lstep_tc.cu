@@ -33,13 +33,54 @@ using namespace ptx;
 constexpr int kThreads = 128;
 constexpr float kLog2e = 1.4426950408889634f;
 
+// packed fp32 pairs (FFMA2 / FADD2 / FMUL2): half the issue slots of the scalar softmax
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+    return (uint64_t)__float_as_uint(lo) | ((uint64_t)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ float lo2(uint64_t v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float hi2(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+__device__ __forceinline__ uint64_t ffma2(uint64_t x, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(x), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t x, uint64_t y) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(x), "l"(y));
+    return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t x, uint64_t y) {
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(x), "l"(y));
+    return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
+#ifndef VMB_TRACE
+#define VMB_TRACE 0
+#endif
+#if VMB_TRACE
+// debug-only per-CTA timeline of unit 0, positions < 1456: [final][pos][event] globaltimer (ns)
+__device__ unsigned long long g_tracel[2][1456][8];
+__device__ int g_tracel_lo[2][1456];
+#define TRACEL(ev) do { if (threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.x < 1456) { \
+    unsigned long long tt_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt_)); \
+    g_tracel[FINAL ? 1 : 0][blockIdx.x][ev] = tt_; } } while (0)
+#else
+#define TRACEL(ev) do { } while (0)
+#endif
+
 struct Params {
     TcLstepArgs a;
     int32_t rows;  // R
 };
 
 struct Layout {
-    uint32_t panel, qb, al, y, cl, bars, slot, bytes;
+    uint32_t panel, qb, al, y, cl, bars, slot, ones, bytes;
     __host__ __device__ Layout(int rows, bool final_mode) {
         panel = (uint32_t)rows * 128u;
         qb = 0;
@@ -47,8 +88,10 @@ struct Layout {
         y = 4 * panel;
         cl = (final_mode ? 6 : 4) * panel;
         bars = cl + 512;
-        slot = bars + 48;
-        bytes = slot + 16;
+        slot = bars + 56;
+        // ITER: 16 K-major rows of bf16 ones (the B operand of the column-sum MMA), 1024-aligned
+        ones = (slot + 16 + 1023u) & ~1023u;
+        bytes = final_mode ? slot + 16 : ones + 4096u;
         // M = 128 MMAs read 128 rows of every K-major A panel (rows >= R are don't-care
         // rows of the accumulator) -- keep those reads inside the allocation.
         const uint32_t a_end = (final_mode ? 3 * panel : panel) + 128u * 128u;
@@ -68,6 +111,7 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
     uint64_t* bar_mma2 = bar_load + 2;
     uint64_t* bar_lo = bar_load + 3;      // aL low half loaded
     uint64_t* bar_mma1b = bar_load + 4;   // S += Qb aL_lo^T done
+    uint64_t* bar_cr = bar_load + 5;      // ITER: column sums L^T 1 done
     uint32_t* slot = reinterpret_cast<uint32_t*>(smem + L.slot);
     float* s_cl = reinterpret_cast<float*>(smem + L.cl);
 
@@ -81,6 +125,7 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
     const uint32_t y_addr = smem_u32(smem + L.y);
     // the per-position scalars first: their global-load latency overlaps the barrier setup,
     // the TMA issue and the TMEM allocation below
+    TRACEL(0);
     const int64_t pos = (int64_t)u * a.b + i;
     const float clv = (t < m) ? __ldg(a.cL + pos * m + t) : 0.f;
     float qnv = 0.f, alnv = 0.f;
@@ -101,6 +146,7 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
             mbar_init(bar_mma2, 1);
             mbar_init(bar_lo, 1);
             mbar_init(bar_mma1b, 1);
+            mbar_init(bar_cr, 1);
             fence_mbar_init();
             // loads first: their latency overlaps the TMEM allocation
             const int qbb = u / a.H, qh = u % a.H;
@@ -117,15 +163,24 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
         __syncwarp();
         tmem_alloc<128>(slot);
     }
-    // cL[i, k] * log2(e) -> smem (all rows of this block share it); columns k >= m get +inf,
+    // -cL[i, k] * log2(e) -> smem (all rows of this block share it); columns k >= m get -inf,
     // so their logits are -inf and their exponentials 0 with no per-element select
-    s_cl[t] = (t < m) ? clv * kLog2e : INFINITY;
+    s_cl[t] = (t < m) ? -clv * kLog2e : -INFINITY;
+    if (!FINAL) {
+        // bf16 ones for the column-sum MMA (read by the tensor core after the L-tile fence)
+        uint4* o4 = reinterpret_cast<uint4*>(smem + L.ones);
+        o4[2 * t] = o4[2 * t + 1] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+    }
     // row k = t of aL needs its low half iff the hi half alone could move an L-step logit by more
     // than kLoBound * 2^-9: qscale Qmax |aL_k| > kLoBound (Cauchy-Schwarz over the block's queries)
     const bool need_lo = a.use_lo && t < m && qnv * (alnv * alnv) > a.lo_thresh2;
     tc_fence_before();
     const int any_lo = __syncthreads_or(need_lo);
     tc_fence_after();
+    TRACEL(1);
+#if VMB_TRACE
+    if (t == 0 && u == 0 && i < 1456) g_tracel_lo[FINAL ? 1 : 0][i] = any_lo;
+#endif
     const uint32_t tmem = *slot;
     const bool leader = (warp == 0) && elect_one();
 
@@ -145,6 +200,7 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
     // ---- softmax of row j = t over k < m   (monarch.hpp:124-138)
     mbar_wait(bar_mma1, 0);
     tc_fence_after();
+    TRACEL(2);
     uint32_t sr[NCH * 32];
     if (any_lo) {
         // aL = hi + lo: S += Qb aL_lo^T for the rows that need it.  GEMM 1 has finished reading
@@ -180,6 +236,7 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
         mbar_wait(bar_mma1b, 0);
         tc_fence_after();
     }
+    float inv_row = 0.f;  // 1 / row sum of row j = t
     if (warp * 32 < R) {  // (a warp past the R rows holds no row of L)
 #pragma unroll
         for (int c = 0; c < NCH; ++c) VMB_TMEM_LD32(tmem + lane_base + c * 32, (sr + c * 32));
@@ -190,42 +247,53 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
 #pragma unroll
             for (int k = NCH * 32 - 16; k < NCH * 32; ++k) s[k] = 0.f;
         }
-        const float sc2 = a.qscale * kLog2e;
-        const float4* c4 = reinterpret_cast<const float4*>(s_cl);
-        // base-2 logits x' = S * qscale * log2e - cL * log2e (k >= m: -inf); four independent
-        // max / sum chains
-        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        // base-2 logits x' = S * qscale * log2e - cL * log2e (k >= m: -inf), in packed pairs;
+        // four independent max / sum chains
+        const uint64_t sc2x2 = pk2(a.qscale * kLog2e, a.qscale * kLog2e);
+        uint64_t* s2 = reinterpret_cast<uint64_t*>(sr);
+        const ulonglong2* ncl = reinterpret_cast<const ulonglong2*>(s_cl);
 #pragma unroll
         for (int k4 = 0; k4 < NCH * 8; ++k4) {
-            const float4 c = c4[k4];
-            s[4 * k4 + 0] = fmaf(s[4 * k4 + 0], sc2, -c.x);
-            s[4 * k4 + 1] = fmaf(s[4 * k4 + 1], sc2, -c.y);
-            s[4 * k4 + 2] = fmaf(s[4 * k4 + 2], sc2, -c.z);
-            s[4 * k4 + 3] = fmaf(s[4 * k4 + 3], sc2, -c.w);
+            const ulonglong2 c = ncl[k4];
+            s2[2 * k4] = ffma2(s2[2 * k4], sc2x2, c.x);
+            s2[2 * k4 + 1] = ffma2(s2[2 * k4 + 1], sc2x2, c.y);
+        }
+        float m4[4] = {s[0], s[1], s[2], s[3]};
 #pragma unroll
-            for (int e = 0; e < 4; ++e) m4[e] = fmaxf(m4[e], s[4 * k4 + e]);
+        for (int k = 4; k < NCH * 32; k += 8) {
+            m4[0] = fmax3(m4[0], s[k + 0], s[k + 1]);
+            m4[1] = fmax3(m4[1], s[k + 2], s[k + 3]);
+            m4[2] = fmax3(m4[2], s[k + 4], s[k + 5]);
+            m4[3] = fmax3(m4[3], s[k + 6], s[k + 7]);
         }
         const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-        float s4[4] = {0.f, 0.f, 0.f, 0.f};
+        const uint64_t negm2 = pk2(-mx, -mx);
+        uint64_t acc[4] = {0, 0, 0, 0};
 #pragma unroll
-        for (int k = 0; k < NCH * 32; ++k) {
-            s[k] = ex2(s[k] - mx);
-            s4[k & 3] += s[k];
+        for (int x = 0; x < NCH * 16; ++x) {
+            const uint64_t t2 = fadd2(s2[x], negm2);
+            s2[x] = pk2(ex2(lo2(t2)), ex2(hi2(t2)));
+            acc[x & 3] = fadd2(acc[x & 3], s2[x]);
         }
-        // rows j >= m are written as zeros: they are part of GEMM 2's K extent (ITER)
-        const float inv = (t < m) ? 1.f / ((s4[0] + s4[1]) + (s4[2] + s4[3])) : 0.f;
+        const uint64_t accs = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+        // rows j >= m are zeros: they are part of GEMM 2's K extent (ITER).  FINAL leaves the
+        // rows unnormalised (E = exp) and scales row j of O = E y by 1/sum in the epilogue.
+        inv_row = (t < m) ? 1.f / (lo2(accs) + hi2(accs)) : 0.f;
+        const uint64_t inv2 = FINAL ? pk2(1.f, 1.f) : pk2(inv_row, inv_row);
         // L row j -> bf16, SW128, over the consumed aL tile
         if (t < R) {
             uint8_t* lt = smem + L.al;
 #pragma unroll
             for (int c8 = 0; c8 < NCH * 4; ++c8) {
                 if (c8 * 8 < R) {
-                    uint4 v;
-                    v.x = pack_bf16(s[8 * c8 + 0] * inv, s[8 * c8 + 1] * inv);
-                    v.y = pack_bf16(s[8 * c8 + 2] * inv, s[8 * c8 + 3] * inv);
-                    v.z = pack_bf16(s[8 * c8 + 4] * inv, s[8 * c8 + 5] * inv);
-                    v.w = pack_bf16(s[8 * c8 + 6] * inv, s[8 * c8 + 7] * inv);
-                    *reinterpret_cast<uint4*>(lt + (c8 >> 3) * L.panel + sw128_offset(t, (c8 & 7) * 8)) = v;
+                    uint32_t w[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const uint64_t q2 = FINAL ? s2[4 * c8 + e] : fmul2(s2[4 * c8 + e], inv2);
+                        w[e] = pack_bf16(lo2(q2), hi2(q2));
+                    }
+                    *reinterpret_cast<uint4*>(lt + (c8 >> 3) * L.panel + sw128_offset(t, (c8 & 7) * 8)) =
+                        make_uint4(w[0], w[1], w[2], w[3]);
                 }
             }
         }
@@ -234,9 +302,36 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    TRACEL(3);
+
+    const uint32_t nk = (uint32_t)R / 16;
+    if (!FINAL) {
+        // cR[k,i] = sum_j L[j,k]  (monarch.hpp:139-143) on the tensor core: L^T 1 with
+        // A = L^T (M=k, K=j) MN-major, B = 16 columns of ones, into TMEM columns [0, 16); read
+        // (lane k = thread t) before GEMM 2 overwrites them
+        if (leader) {
+            const uint32_t ones_addr = smem_u32(smem + L.ones);
+            const uint32_t idc = idesc_bf16(128, 16, 1, 0);
+            for (uint32_t kk = 0; kk < nk; ++kk)
+                umma_ss(tmem, sdesc_sw128(al_addr + kk * 2048, L.panel, 1024),
+                        sdesc_sw128(ones_addr + (kk & 3) * 32, 16, 1024), idc, kk > 0);
+            umma_commit(bar_cr);
+        }
+        __syncwarp();
+        mbar_wait(bar_cr, 0);
+        tc_fence_after();
+        if (warp * 32 < m) {
+            uint32_t v;
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(tmem + lane_base));
+            tmem_ld_wait();
+            if (t < m) a.cR[((int64_t)u * m + t) * a.b + i] = __uint_as_float(v);
+        }
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+    }
 
     if (leader) {
-        const uint32_t nk = (uint32_t)R / 16;
         if (!FINAL) {
             // aR' = L^T [Qb]: A = L^T (M=k, K=j) MN-major, B = Qb (K=j, N=d) MN-major
             const uint32_t id2 = idesc_bf16(128, 128, 1, 1);
@@ -244,7 +339,8 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
                 umma_ss(tmem, sdesc_sw128(al_addr + kk * 2048, L.panel, 1024),
                         sdesc_sw128(qb_addr + kk * 2048, L.panel, 1024), id2, kk > 0);
         } else {
-            // O_i = L Y: A = L (M=j, K=k) K-major, B = Y (K=k, N=d) MN-major
+            // O_i = E Y (E: unnormalised rows of L): A = E (M=j, K=k) K-major, B = Y (K=k, N=d)
+            // MN-major
             const uint32_t id2 = idesc_bf16(128, 128, 0, 1);
             for (uint32_t kk = 0; kk < nk; ++kk) {
                 const uint32_t off = (kk >> 2) * L.panel + (kk & 3) * 32;
@@ -256,50 +352,12 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
     }
     __syncwarp();
 
-    if (!FINAL) {
-        // cR[k,i] = sum_j L[j,k]  (monarch.hpp:139-143) from the bf16 copy of L, while GEMM 2
-        // runs: thread t sums the column pair (2p, 2p+1), p = t % 64, over half the rows (t < 64:
-        // j < mh, else j >= mh); 32-bit loads, four independent chains per column
-        const int p = t & 63, half = t >> 6;
-        const int mh = (m + 1) >> 1;
-        const int j0 = half ? mh : 0, j1 = half ? m : mh;
-        float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
-        if (2 * p < m) {
-            const uint8_t* base = smem + L.al + (p >> 5) * L.panel;
-            const uint32_t col = (2 * p) & 63;
-            int j = j0;
-            for (; j + 4 <= j1; j += 4) {
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const uint32_t w = *reinterpret_cast<const uint32_t*>(base + sw128_offset(j + e, col));
-                    c0[e] += __uint_as_float(w << 16);
-                    c1[e] += __uint_as_float(w & 0xFFFF0000u);
-                }
-            }
-            for (; j < j1; ++j) {
-                const uint32_t w = *reinterpret_cast<const uint32_t*>(base + sw128_offset(j, col));
-                c0[0] += __uint_as_float(w << 16);
-                c1[0] += __uint_as_float(w & 0xFFFF0000u);
-            }
-        }
-        const float cs0 = (c0[0] + c0[1]) + (c0[2] + c0[3]);
-        const float cs1 = (c1[0] + c1[1]) + (c1[2] + c1[3]);
-        // the upper half hands its partial sums over through the (consumed) cL slots
-        float2* part = reinterpret_cast<float2*>(s_cl);
-        if (half) part[p] = make_float2(cs0, cs1);
-        __syncthreads();
-        if (!half && 2 * p < m) {
-            const float2 q = part[p];
-            float* cr = a.cR + ((int64_t)u * m + 2 * p) * a.b + i;
-            cr[0] = cs0 + q.x;
-            if (2 * p + 1 < m) cr[a.b] = cs1 + q.y;
-        }
-    }
-
     // ---- epilogue: TMEM row t -> bf16 SW128 staging tile over Qb -> TMA store
+    TRACEL(4);
     mbar_wait(bar_mma2, 0);
     tc_fence_after();
-    const float scale = a.out_scale;
+    TRACEL(5);
+    const float scale = FINAL ? a.out_scale * inv_row : a.out_scale;
 #pragma unroll
     for (int cc = 0; cc < 4; ++cc) {
         if (warp * 32 >= R) break;  // no output row in this warp
@@ -322,6 +380,7 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
     fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
+    TRACEL(6);
     if (t == 0) {
         if (!FINAL) {
             tma_store_5d(&a.tmOut, smem + L.qb, 0, i, 0, 0, u);
@@ -333,6 +392,7 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
         }
         tma_store_commit();
         tma_store_wait_read();
+        TRACEL(7);
     }
     if (warp == 0) {
         __syncwarp();
@@ -641,6 +701,15 @@ void launch(const Params& p, int64_t U, cudaStream_t s) {
 }
 
 }  // namespace
+
+#if VMB_TRACE
+extern "C" int vmb_debug_tracel_read(unsigned long long* host) {
+    return cudaMemcpyFromSymbol(host, g_tracel, sizeof(unsigned long long) * 2 * 1456 * 8) == cudaSuccess ? 0 : -1;
+}
+extern "C" int vmb_debug_tracel_lo_read(int* host) {
+    return cudaMemcpyFromSymbol(host, g_tracel_lo, sizeof(int) * 2 * 1456) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 void tc_lstep_hl_launch(const TcLstepHlArgs& a, int64_t U, cudaStream_t s) {
     if (U == 0 || a.b == 0) return;
