@@ -74,6 +74,11 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t x, uint64_t y) {
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(x), "l"(y));
     return d;
 }
+__device__ __forceinline__ uint64_t fmul2(uint64_t x, uint64_t y) {
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(x), "l"(y));
+    return d;
+}
 __device__ __forceinline__ uint64_t pk2(float lo, float hi) {
     return (uint64_t)__float_as_uint(lo) | ((uint64_t)__float_as_uint(hi) << 32);
 }
@@ -542,8 +547,12 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                 mbar_arrive(&o_empty[ob]);
                 if (valid) a.part_lse[((int64_t)w.useg * a.nsplit + w.split) * a.q_len + grow] = kLn2 * lse2;
             } else {
-                float qo = 0.f;   // <q_row, (P K)_row> (R-step entropy)
-                float ssa = 0.f;  // |aL row|^2: decides its low half and feeds aln_out
+                // packed pairs throughout: the epilogue shares each SMSP's issue slots with the
+                // next item's softmax warp, so its instruction count is the drain time
+                uint64_t qo2 = 0;   // <q_row, (P K)_row> (R-step entropy), lane pairs
+                uint64_t ss2 = 0;   // |(P K)_row|^2 before normalisation, lane pairs
+                const uint64_t inv2 = pk2(inv_l, inv_l);
+                float ssa = 0.f;    // |aL row|^2: decides its low half and feeds aln_out
                 const int64_t obh = w.u / a.oHn, ohh = w.u % a.oHn;
 #pragma unroll
                 for (int t = 0; t < NO; ++t) {
@@ -560,33 +569,28 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                             mbar_arrive(&o_empty[ob]);
                             if (threadIdx.x == 192) TRACE4(n, 5);
                         }
+                        const uint64_t* o2 = reinterpret_cast<const uint64_t*>(orr);
                         if (t == 0 && a.cl_out) {
 #pragma unroll
                             for (int x = 0; x < 4; ++x) {
                                 const uint4 q4 = qv[cc * 4 + x];
                                 const uint32_t qw[4] = {q4.x, q4.y, q4.z, q4.w};
 #pragma unroll
-                                for (int e = 0; e < 4; ++e) {
-                                    qo = fmaf(__uint_as_float(qw[e] << 16), __uint_as_float(orr[8 * x + 2 * e]), qo);
-                                    qo = fmaf(__uint_as_float(qw[e] & 0xFFFF0000u), __uint_as_float(orr[8 * x + 2 * e + 1]), qo);
-                                }
+                                for (int e = 0; e < 4; ++e)
+                                    qo2 = ffma2((uint64_t)(qw[e] << 16) | ((uint64_t)(qw[e] & 0xFFFF0000u) << 32), o2[4 * x + e], qo2);
                             }
                         }
                         if (valid) {
-                            float f[32];
+                            uint32_t w16[16];
 #pragma unroll
-                            for (int x = 0; x < 32; ++x) {
-                                f[x] = __uint_as_float(orr[x]) * inv_l;
-                                if (t == 0) ssa = fmaf(f[x], f[x], ssa);
+                            for (int x = 0; x < 16; ++x) {
+                                if (t == 0) ss2 = ffma2(o2[x], o2[x], ss2);
+                                const uint64_t nrm = fmul2(o2[x], inv2);
+                                w16[x] = pack_bf16(lo2(nrm), hi2(nrm));
                             }
                             uint4 v[4];
 #pragma unroll
-                            for (int x = 0; x < 4; ++x) {
-                                v[x].x = pack_bf16(__uint_as_float(orr[8 * x + 0]) * inv_l, __uint_as_float(orr[8 * x + 1]) * inv_l);
-                                v[x].y = pack_bf16(__uint_as_float(orr[8 * x + 2]) * inv_l, __uint_as_float(orr[8 * x + 3]) * inv_l);
-                                v[x].z = pack_bf16(__uint_as_float(orr[8 * x + 4]) * inv_l, __uint_as_float(orr[8 * x + 5]) * inv_l);
-                                v[x].w = pack_bf16(__uint_as_float(orr[8 * x + 6]) * inv_l, __uint_as_float(orr[8 * x + 7]) * inv_l);
-                            }
+                            for (int x = 0; x < 4; ++x) v[x] = make_uint4(w16[4 * x], w16[4 * x + 1], w16[4 * x + 2], w16[4 * x + 3]);
                             if (VMB_DEBUG_NO_STORE) {
                                 asm volatile("" ::"r"(v[0].x), "r"(v[1].y), "r"(v[2].z), "r"(v[3].w));
                             } else if (a.out_align32) {
@@ -604,6 +608,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                     // not known yet -> every row), a second TMEM pass so the entropy dot's
                     // prefetched q row is dead by then (register budget).  tcgen05.ld is
                     // warp-collective: a warp with any such row loads, only those rows store.
+                    if (t == 0) ssa = (lo2(ss2) + hi2(ss2)) * (inv_l * inv_l);
                     const bool need_lo =
                         valid && (a.qn == nullptr || a.qn[(int64_t)w.u * a.q_len + grow] * ssa > a.lo_thresh2);
                     if (t == 0 && a.out0_lo && NO == 1 && !__any_sync(0xffffffffu, need_lo)) {
@@ -652,7 +657,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa4_kernel(const __grid_constant_
                 }
                 if (valid) {
                     if (a.cl_out)
-                        a.cl_out[((int64_t)w.u * a.q_len + grow) * a.nseg + w.seg] = kLn2 * (scale2 * qo * inv_l - lse2);
+                        a.cl_out[((int64_t)w.u * a.q_len + grow) * a.nseg + w.seg] = kLn2 * (scale2 * (lo2(qo2) + hi2(qo2)) * inv_l - lse2);
                     if (a.aln_out) a.aln_out[((int64_t)w.u * a.q_len + grow) * a.nseg + w.seg] = sqrtf(ssa);
                     if (a.lse_out) a.lse_out[((int64_t)w.u * a.nseg + w.seg) * a.q_len + grow] = kLn2 * lse2;
                 }
