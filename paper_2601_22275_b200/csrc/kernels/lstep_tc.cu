@@ -85,8 +85,9 @@ struct Layout {
         panel = (uint32_t)rows * 128u;
         qb = 0;
         al = 2 * panel;
-        y = 4 * panel;
-        cl = (final_mode ? 6 : 4) * panel;
+        // FINAL: y lands over Qb once GEMM 1 has consumed it (four CTAs per SM instead of three)
+        y = 0;
+        cl = 4 * panel;
         bars = cl + 512;
         slot = bars + 56;
         // ITER: 16 K-major rows of bf16 ones (the B operand of the column-sum MMA), 1024-aligned
@@ -100,7 +101,7 @@ struct Layout {
 };
 
 template <bool FINAL, int NCH>
-__global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lstep_tc_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : 4) lstep_tc_kernel(const __grid_constant__ Params p) {
     const TcLstepArgs& a = p.a;
     const int R = p.rows;
     const Layout L(R, FINAL);
@@ -112,6 +113,7 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
     uint64_t* bar_lo = bar_load + 3;      // aL low half loaded
     uint64_t* bar_mma1b = bar_load + 4;   // S += Qb aL_lo^T done
     uint64_t* bar_cr = bar_load + 5;      // ITER: column sums L^T 1 done
+    uint64_t* bar_y = bar_load + 6;       // FINAL: y loaded (over Qb, after GEMM 1)
     uint32_t* slot = reinterpret_cast<uint32_t*>(smem + L.slot);
     float* s_cl = reinterpret_cast<float*>(smem + L.cl);
 
@@ -147,18 +149,15 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
             mbar_init(bar_lo, 1);
             mbar_init(bar_mma1b, 1);
             mbar_init(bar_cr, 1);
+            mbar_init(bar_y, 1);
             fence_mbar_init();
             // loads first: their latency overlaps the TMEM allocation
             const int qbb = u / a.H, qh = u % a.H;
-            mbar_arrive_expect_tx(bar_load, (FINAL ? 6u : 4u) * L.panel);
+            mbar_arrive_expect_tx(bar_load, 4u * L.panel);
             tma_load_5d(smem + L.qb, &a.tmQ, bar_load, 0, i, 0, qh, qbb);
             tma_load_5d(smem + L.qb + L.panel, &a.tmQ, bar_load, 64, i, 0, qh, qbb);
             tma_load_5d(smem + L.al, &a.tmAL, bar_load, 0, 0, i, 0, u);
             tma_load_5d(smem + L.al + L.panel, &a.tmAL, bar_load, 64, 0, i, 0, u);
-            if (FINAL) {
-                tma_load_5d(smem + L.y, &a.tmY, bar_load, 0, i, 0, 0, u);
-                tma_load_5d(smem + L.y + L.panel, &a.tmY, bar_load, 64, i, 0, 0, u);
-            }
         }
         __syncwarp();
         tmem_alloc<128>(slot);
@@ -201,6 +200,15 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
     mbar_wait(bar_mma1, 0);
     tc_fence_after();
     TRACEL(2);
+    // FINAL: Qb is consumed (unless the low-half pass still reads it): y goes over it
+    auto load_y = [&]() {
+        if (FINAL && leader) {
+            mbar_arrive_expect_tx(bar_y, 2u * L.panel);
+            tma_load_5d(smem + L.y, &a.tmY, bar_y, 0, i, 0, 0, u);
+            tma_load_5d(smem + L.y + L.panel, &a.tmY, bar_y, 64, i, 0, 0, u);
+        }
+    };
+    if (!any_lo) load_y();
     uint32_t sr[NCH * 32];
     if (any_lo) {
         // aL = hi + lo: S += Qb aL_lo^T for the rows that need it.  GEMM 1 has finished reading
@@ -235,6 +243,7 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
         __syncwarp();
         mbar_wait(bar_mma1b, 0);
         tc_fence_after();
+        load_y();
     }
     float inv_row = 0.f;  // 1 / row sum of row j = t
     if (warp * 32 < R) {  // (a warp past the R rows holds no row of L)
@@ -341,6 +350,8 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : (FINAL ? 3 : 4)) lste
         } else {
             // O_i = E Y (E: unnormalised rows of L): A = E (M=j, K=k) K-major, B = Y (K=k, N=d)
             // MN-major
+            mbar_wait(bar_y, 0);
+            tc_fence_after();
             const uint32_t id2 = idesc_bf16(128, 128, 0, 1);
             for (uint32_t kk = 0; kk < nk; ++kk) {
                 const uint32_t off = (kk >> 2) * L.panel + (kk & 3) * 32;
