@@ -49,6 +49,18 @@ constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescaleThreshold = 8.0f;
 constexpr float kMasked = -1.0e30f;
 
+#ifndef VMB_TRACE
+#define VMB_TRACE 0
+#endif
+#if VMB_TRACE
+// debug-only per-CTA timeline of the first 4096 CTAs of a launch: [cta][event] globaltimer (ns)
+__device__ unsigned long long g_trace2[4096][8];
+#define TRACE2(ev) do { if (blockIdx.x < 4096) { unsigned long long tt_; \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt_)); g_trace2[blockIdx.x][ev] = tt_; } } while (0)
+#else
+#define TRACE2(ev) do { } while (0)
+#endif
+
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
     float d;
     asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
@@ -69,6 +81,11 @@ struct Params {
 __device__ __forceinline__ uint64_t ffma2(uint64_t x, uint64_t b, uint64_t c) {
     uint64_t d;
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(x), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t x, uint64_t y) {
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(x), "l"(y));
     return d;
 }
 __device__ __forceinline__ uint64_t fadd2(uint64_t x, uint64_t y) {
@@ -147,6 +164,7 @@ __global__ void __launch_bounds__(kThreads, HL ? 1 : 2) fa2_kernel(const __grid_
     const int kv_tile0 = split * p.n_kv_tiles;
     const int n_kv = min(p.n_kv_tiles, p.total_tiles - kv_tile0);
 
+    if (threadIdx.x == 0 && !HL) TRACE2(0);
     if (warp == 0 && elect_one()) {
         tma_prefetch_desc(&a.tmQ);
         tma_prefetch_desc(&a.tmK);
@@ -322,10 +340,12 @@ __global__ void __launch_bounds__(kThreads, HL ? 1 : 2) fa2_kernel(const __grid_
 
         float m_run = -INFINITY, l_run = 0.f;
         const uint64_t scale2x2 = pk2(scale2, scale2);
+        if (threadIdx.x == 64 && !HL) TRACE2(1);
         for (int j = 0; j < n_kv; ++j) {
             const uint32_t tS = tS0 + (j & 1) * kBN + lane_base;
             mbar_wait_sleep(&s_full[j & 1], (j >> 1) & 1);
             tc_fence_after();
+            if (threadIdx.x == 64 && !HL && j == 0) TRACE2(2);
 #if VMB_DEBUG_NO_SOFTMAX  // timing experiment only: MMA/TMA pipeline without the softmax
             if (true) {
                 mbar_arrive(&p_full[j & 1]);
@@ -427,8 +447,10 @@ __global__ void __launch_bounds__(kThreads, HL ? 1 : 2) fa2_kernel(const __grid_
         }
 
         // ------------------------------------------------------------ epilogue
+        if (threadIdx.x == 64 && !HL) TRACE2(3);
         mbar_wait_sleep(o_full, 0);
         tc_fence_after();
+        if (threadIdx.x == 64 && !HL) TRACE2(4);
         const float inv_l = 1.f / l_run;
         const float lse2 = m_run + log2f(l_run);  // base-2 log-sum-exp of x' = s * scale2
         float qo = 0.f;                            // <q_row, O_row> (R-step entropy)
@@ -463,12 +485,27 @@ __global__ void __launch_bounds__(kThreads, HL ? 1 : 2) fa2_kernel(const __grid_
             __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(a.out) + ob * a.oB + oh * a.oH + (int64_t)seg * a.oS +
                                   (int64_t)grow * a.oR;
             float ssa = 0.f;  // |output row|^2 (aln_out)
+            // bf16 rows in packed pairs (FMUL2 / FFMA2): the epilogue shares issue slots with the
+            // other CTA's softmax warps on the SM
+            uint64_t ss2 = 0, qo2 = 0;
+            const uint64_t inv2 = pk2(inv_l, inv_l);
 #pragma unroll
             for (int cc = 0; cc < 4; ++cc) {
                 uint32_t orr[32];
                 VMB_TMEM_LD32(tO + cc * 32 + lane_base, orr);
                 tmem_ld_wait();
-                if (a.cl_out) {
+                const uint64_t* o2 = reinterpret_cast<const uint64_t*>(orr);
+                if (!HL && a.cl_out) {
+                    const uint8_t* qp = smem + SM::q_off + (cc >> 1) * kQPanel;
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) {
+                        const uint4 qv = *reinterpret_cast<const uint4*>(qp + sw128_offset(row, (cc & 1) * 32 + 8 * x));
+                        const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            qo2 = ffma2((uint64_t)(qw[e] << 16) | ((uint64_t)(qw[e] & 0xFFFF0000u) << 32), o2[4 * x + e], qo2);
+                    }
+                } else if (a.cl_out) {
 #pragma unroll
                     for (int hl = 0; hl < (HL ? 2 : 1); ++hl) {  // HL: q = q_hi + q_lo
                         const uint8_t* qp = smem + SM::q_off + (2 * hl + (cc >> 1)) * kQPanel;
@@ -509,20 +546,17 @@ __global__ void __launch_bounds__(kThreads, HL ? 1 : 2) fa2_kernel(const __grid_
                         }
                     }
                 } else if (valid) {
-                    float f[32];
+                    uint64_t nrm[16];
+                    uint32_t w16[16];
 #pragma unroll
-                    for (int x = 0; x < 32; ++x) {
-                        f[x] = __uint_as_float(orr[x]) * inv_l;
-                        ssa = fmaf(f[x], f[x], ssa);
+                    for (int x = 0; x < 16; ++x) {
+                        ss2 = ffma2(o2[x], o2[x], ss2);
+                        nrm[x] = fmul2(o2[x], inv2);
+                        w16[x] = pack_bf16(lo2(nrm[x]), hi2(nrm[x]));
                     }
                     uint4 v[4];
 #pragma unroll
-                    for (int x = 0; x < 4; ++x) {
-                        v[x].x = pack_bf16(__uint_as_float(orr[8 * x + 0]) * inv_l, __uint_as_float(orr[8 * x + 1]) * inv_l);
-                        v[x].y = pack_bf16(__uint_as_float(orr[8 * x + 2]) * inv_l, __uint_as_float(orr[8 * x + 3]) * inv_l);
-                        v[x].z = pack_bf16(__uint_as_float(orr[8 * x + 4]) * inv_l, __uint_as_float(orr[8 * x + 5]) * inv_l);
-                        v[x].w = pack_bf16(__uint_as_float(orr[8 * x + 6]) * inv_l, __uint_as_float(orr[8 * x + 7]) * inv_l);
-                    }
+                    for (int x = 0; x < 4; ++x) v[x] = make_uint4(w16[4 * x], w16[4 * x + 1], w16[4 * x + 2], w16[4 * x + 3]);
                     if (a.out_align32) {  // 256-bit stores: one full sector per instruction
                         st_global_256(orow + cc * 32, v[0], v[1]);
                         st_global_256(orow + cc * 32 + 16, v[2], v[3]);
@@ -532,14 +566,15 @@ __global__ void __launch_bounds__(kThreads, HL ? 1 : 2) fa2_kernel(const __grid_
                         for (int x = 0; x < 4; ++x) dst[x] = v[x];
                     }
                     if (a.out_lo) {
-                        // low half of aL (same layout): bf16(x - bf16(x))
+                        // low half of aL (same layout): bf16(x - bf16(x)), the residual in packed pairs
 #pragma unroll
-                        for (int x = 0; x < 4; ++x) {
-                            v[x].x = pack_bf16_residual(__uint_as_float(orr[8 * x + 0]) * inv_l, __uint_as_float(orr[8 * x + 1]) * inv_l, v[x].x);
-                            v[x].y = pack_bf16_residual(__uint_as_float(orr[8 * x + 2]) * inv_l, __uint_as_float(orr[8 * x + 3]) * inv_l, v[x].y);
-                            v[x].z = pack_bf16_residual(__uint_as_float(orr[8 * x + 4]) * inv_l, __uint_as_float(orr[8 * x + 5]) * inv_l, v[x].z);
-                            v[x].w = pack_bf16_residual(__uint_as_float(orr[8 * x + 6]) * inv_l, __uint_as_float(orr[8 * x + 7]) * inv_l, v[x].w);
+                        for (int x = 0; x < 16; ++x) {
+                            const uint64_t hi2v = (uint64_t)(w16[x] << 16) | ((uint64_t)(w16[x] & 0xFFFF0000u) << 32);
+                            const uint64_t r2 = fadd2(nrm[x], hi2v ^ 0x8000000080000000ull);
+                            w16[x] = pack_bf16(lo2(r2), hi2(r2));
                         }
+#pragma unroll
+                        for (int x = 0; x < 4; ++x) v[x] = make_uint4(w16[4 * x], w16[4 * x + 1], w16[4 * x + 2], w16[4 * x + 3]);
                         __nv_bfloat16* lrow = static_cast<__nv_bfloat16*>(a.out_lo) + (orow - static_cast<__nv_bfloat16*>(a.out));
                         if (a.out_align32) {
                             st_global_256(lrow + cc * 32, v[0], v[1]);
@@ -552,6 +587,8 @@ __global__ void __launch_bounds__(kThreads, HL ? 1 : 2) fa2_kernel(const __grid_
                     }
                 }
             }
+            if (!HL) qo += lo2(qo2) + hi2(qo2);
+            ssa = (lo2(ss2) + hi2(ss2)) * (inv_l * inv_l);
             if (valid) {
                 if (a.cl_out)
                     a.cl_out[((int64_t)u * a.q_len + grow) * a.nseg + seg] = kLn2 * (scale2 * qo * inv_l - lse2);
@@ -561,8 +598,10 @@ __global__ void __launch_bounds__(kThreads, HL ? 1 : 2) fa2_kernel(const __grid_
         }
     }
 
+    if (threadIdx.x == 64 && !HL) TRACE2(5);
     tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0 && !HL) TRACE2(6);
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc<256>(tmem);
@@ -705,3 +744,9 @@ void tc2_combine_launch(const Tc2Args& a, cudaStream_t s) {
 }
 
 }  // namespace vmb
+
+#if VMB_TRACE
+extern "C" int vmb_debug_trace2_read(unsigned long long* host) {
+    return cudaMemcpyFromSymbol(host, vmb::g_trace2, sizeof(unsigned long long) * 4096 * 8) == cudaSuccess ? 0 : -1;
+}
+#endif
