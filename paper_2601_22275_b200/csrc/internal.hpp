@@ -252,6 +252,13 @@ void tc4_fa_launch(Tc4Args a, int64_t U, cudaStream_t s);
 // All L-step tiles are boxes of `rows = lstep_rows(m)` rows (m rounded up to 16); rows
 // >= m are OOB (zero-filled on load, clipped on store).
 inline int32_t lstep_rows(int64_t m) { return (int32_t)((m + 15) & ~int64_t(15)); }
+// bf16 tcgen05 L-step (lstep_tc.cu): spatial positions per CTA (stacked in the 128 tile rows)
+// and the rows per position of its TMA boxes (the maps of Qb, aL, y, aR and O use these)
+inline int32_t lstep_positions(int64_t m) { return m <= 32 ? 4 : (m <= 64 ? 2 : 1); }
+inline int32_t lstep_box_rows(int64_t m) {
+    const int32_t P = lstep_positions(m);
+    return P > 1 ? 128 / P : lstep_rows(m);
+}
 struct TcLstepArgs {
     CUtensorMap tmQ;    // Q rows, 5-D (d, i, j, head, batch): Qb[i][j], box (64, 1, rows)
     CUtensorMap tmAL;   // aL rows, 5-D (d, k, i, 1, unit), box (64, rows, 1)

@@ -100,11 +100,18 @@ struct Layout {
     }
 };
 
-template <bool FINAL, int NCH>
+// P positions per CTA (m <= 32: 4, m <= 64: 2, else 1).  With P > 1 the positions' tiles are
+// stacked in the 128 tile rows (position p in rows [p R, p R + R), R = 128 / P) and the
+// products are block-diagonal: GEMM 1 computes every cross-position block as well (the
+// softmax reads only its own), L is written with zeros outside its diagonal block, so GEMM 2
+// and the column sums need no masking.  Small m then keeps the tensor tiles and the bytes in
+// flight per CTA as large as at m = 128.
+template <bool FINAL, int NCH, int P>
 __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : 4) lstep_tc_kernel(const __grid_constant__ Params p) {
     const TcLstepArgs& a = p.a;
-    const int R = p.rows;
-    const Layout L(R, FINAL);
+    const int R = p.rows;                       // rows per position
+    const int RT = P * R;                       // stacked rows (P > 1: 128)
+    const Layout L(RT, FINAL);
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
     uint64_t* bar_load = reinterpret_cast<uint64_t*>(smem + L.bars);
@@ -117,10 +124,14 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : 4) lstep_tc_kernel(co
     uint32_t* slot = reinterpret_cast<uint32_t*>(smem + L.slot);
     float* s_cl = reinterpret_cast<float*>(smem + L.cl);
 
-    const int i = blockIdx.x, u = blockIdx.y;
+    const int i = blockIdx.x * P, u = blockIdx.y;  // first position of this CTA
     const int m = a.m;
     const int warp = warp_id();
     const int t = threadIdx.x;
+    // thread t = stacked row t: position pi (i + pi), row rr within it
+    const int pi = P == 1 ? 0 : t / R;
+    const int rr = P == 1 ? t : t % R;
+    const bool pos_ok = i + pi < a.b;
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
     const uint32_t qb_addr = smem_u32(smem + L.qb);
     const uint32_t al_addr = smem_u32(smem + L.al);
@@ -128,12 +139,13 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : 4) lstep_tc_kernel(co
     // the per-position scalars first: their global-load latency overlaps the barrier setup,
     // the TMA issue and the TMEM allocation below
     TRACEL(0);
-    const int64_t pos = (int64_t)u * a.b + i;
-    const float clv = (t < m) ? __ldg(a.cL + pos * m + t) : 0.f;
+    const int64_t pos = (int64_t)u * a.b + i + pi;
+    const bool row_ok = rr < m && pos_ok;
+    const float clv = row_ok ? __ldg(a.cL + pos * m + rr) : 0.f;
     float qnv = 0.f, alnv = 0.f;
-    if (a.use_lo && t < m) {
+    if (a.use_lo && row_ok) {
         qnv = __ldg(a.qn + pos);
-        alnv = __ldg(a.aln + pos * m + t);
+        alnv = __ldg(a.aln + pos * m + rr);
     }
 
     if (warp == 0) {
@@ -154,17 +166,21 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : 4) lstep_tc_kernel(co
             // loads first: their latency overlaps the TMEM allocation
             const int qbb = u / a.H, qh = u % a.H;
             mbar_arrive_expect_tx(bar_load, 4u * L.panel);
-            tma_load_5d(smem + L.qb, &a.tmQ, bar_load, 0, i, 0, qh, qbb);
-            tma_load_5d(smem + L.qb + L.panel, &a.tmQ, bar_load, 64, i, 0, qh, qbb);
-            tma_load_5d(smem + L.al, &a.tmAL, bar_load, 0, 0, i, 0, u);
-            tma_load_5d(smem + L.al + L.panel, &a.tmAL, bar_load, 64, 0, i, 0, u);
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+                const uint32_t o = (uint32_t)(q * R) * 128u;
+                tma_load_5d(smem + L.qb + o, &a.tmQ, bar_load, 0, i + q, 0, qh, qbb);
+                tma_load_5d(smem + L.qb + L.panel + o, &a.tmQ, bar_load, 64, i + q, 0, qh, qbb);
+                tma_load_5d(smem + L.al + o, &a.tmAL, bar_load, 0, 0, i + q, 0, u);
+                tma_load_5d(smem + L.al + L.panel + o, &a.tmAL, bar_load, 64, 0, i + q, 0, u);
+            }
         }
         __syncwarp();
         tmem_alloc<128>(slot);
     }
     // -cL[i, k] * log2(e) -> smem (all rows of this block share it); columns k >= m get -inf,
     // so their logits are -inf and their exponentials 0 with no per-element select
-    s_cl[t] = (t < m) ? -clv * kLog2e : -INFINITY;
+    s_cl[t] = row_ok ? -clv * kLog2e : -INFINITY;
     if (!FINAL) {
         // bf16 ones for the column-sum MMA (read by the tensor core after the L-tile fence)
         uint4* o4 = reinterpret_cast<uint4*>(smem + L.ones);
@@ -172,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : 4) lstep_tc_kernel(co
     }
     // row k = t of aL needs its low half iff the hi half alone could move an L-step logit by more
     // than kLoBound * 2^-9: qscale Qmax |aL_k| > kLoBound (Cauchy-Schwarz over the block's queries)
-    const bool need_lo = a.use_lo && t < m && qnv * (alnv * alnv) > a.lo_thresh2;
+    const bool need_lo = a.use_lo && row_ok && qnv * (alnv * alnv) > a.lo_thresh2;
     tc_fence_before();
     const int any_lo = __syncthreads_or(need_lo);
     tc_fence_after();
@@ -186,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : 4) lstep_tc_kernel(co
     if (leader) {
         mbar_wait(bar_load, 0);
         tc_fence_after();
-        const uint32_t id1 = idesc_bf16(128, (uint32_t)R, 0, 0);
+        const uint32_t id1 = idesc_bf16(128, (uint32_t)RT, 0, 0);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
             const uint32_t off = (kk >> 2) * L.panel + (kk & 3) * 32;
@@ -204,8 +220,12 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : 4) lstep_tc_kernel(co
     auto load_y = [&]() {
         if (FINAL && leader) {
             mbar_arrive_expect_tx(bar_y, 2u * L.panel);
-            tma_load_5d(smem + L.y, &a.tmY, bar_y, 0, i, 0, 0, u);
-            tma_load_5d(smem + L.y + L.panel, &a.tmY, bar_y, 64, i, 0, 0, u);
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+                const uint32_t o = (uint32_t)(q * R) * 128u;
+                tma_load_5d(smem + L.y + o, &a.tmY, bar_y, 0, i + q, 0, 0, u);
+                tma_load_5d(smem + L.y + L.panel + o, &a.tmY, bar_y, 64, i + q, 0, 0, u);
+            }
         }
     };
     if (!any_lo) load_y();
@@ -216,12 +236,16 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : 4) lstep_tc_kernel(co
         // did not write (or does not matter) are zeroed before the MMA reads the tile.
         if (leader) {
             mbar_arrive_expect_tx(bar_lo, 2u * L.panel);
-            tma_load_5d(smem + L.al, &a.tmALlo, bar_lo, 0, 0, i, 0, u);
-            tma_load_5d(smem + L.al + L.panel, &a.tmALlo, bar_lo, 64, 0, i, 0, u);
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+                const uint32_t o = (uint32_t)(q * R) * 128u;
+                tma_load_5d(smem + L.al + o, &a.tmALlo, bar_lo, 0, 0, i + q, 0, u);
+                tma_load_5d(smem + L.al + L.panel + o, &a.tmALlo, bar_lo, 64, 0, i + q, 0, u);
+            }
         }
         __syncwarp();
         mbar_wait(bar_lo, 0);
-        if (t < R && !need_lo) {
+        if (t < RT && !need_lo) {
             uint4* r0 = reinterpret_cast<uint4*>(smem + L.al + t * 128);
             uint4* r1 = reinterpret_cast<uint4*>(smem + L.al + L.panel + t * 128);
 #pragma unroll
@@ -232,7 +256,7 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : 4) lstep_tc_kernel(co
         __syncthreads();
         tc_fence_after();
         if (leader) {
-            const uint32_t id1 = idesc_bf16(128, (uint32_t)R, 0, 0);
+            const uint32_t id1 = idesc_bf16(128, (uint32_t)RT, 0, 0);
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
                 const uint32_t off = (kk >> 2) * L.panel + (kk & 3) * 32;
@@ -246,9 +270,11 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : 4) lstep_tc_kernel(co
         load_y();
     }
     float inv_row = 0.f;  // 1 / row sum of row j = t
-    if (warp * 32 < R) {  // (a warp past the R rows holds no row of L)
+    if (warp * 32 < RT) {  // (a warp past the R rows holds no row of L)
+        // this row's own block of the score tile: columns [pi R, pi R + R)
+        const uint32_t tcol = tmem + lane_base + (uint32_t)(pi * R);
 #pragma unroll
-        for (int c = 0; c < NCH; ++c) VMB_TMEM_LD32(tmem + lane_base + c * 32, (sr + c * 32));
+        for (int c = 0; c < NCH; ++c) VMB_TMEM_LD32(tcol + c * 32, (sr + c * 32));
         tmem_ld_wait();
         float* s = reinterpret_cast<float*>(sr);
         // R = NCH*32 - 16: TMEM columns [R, NCH*32) are not written by GEMM 1 (don't-care data)
@@ -260,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : 4) lstep_tc_kernel(co
         // four independent max / sum chains
         const uint64_t sc2x2 = pk2(a.qscale * kLog2e, a.qscale * kLog2e);
         uint64_t* s2 = reinterpret_cast<uint64_t*>(sr);
-        const ulonglong2* ncl = reinterpret_cast<const ulonglong2*>(s_cl);
+        const ulonglong2* ncl = reinterpret_cast<const ulonglong2*>(s_cl + pi * R);
 #pragma unroll
         for (int k4 = 0; k4 < NCH * 8; ++k4) {
             const ulonglong2 c = ncl[k4];
@@ -287,10 +313,32 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : 4) lstep_tc_kernel(co
         const uint64_t accs = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
         // rows j >= m are zeros: they are part of GEMM 2's K extent (ITER).  FINAL leaves the
         // rows unnormalised (E = exp) and scales row j of O = E y by 1/sum in the epilogue.
-        inv_row = (t < m) ? 1.f / (lo2(accs) + hi2(accs)) : 0.f;
+        inv_row = row_ok ? 1.f / (lo2(accs) + hi2(accs)) : 0.f;
         const uint64_t inv2 = FINAL ? pk2(1.f, 1.f) : pk2(inv_row, inv_row);
         // L row j -> bf16, SW128, over the consumed aL tile
-        if (t < R) {
+        if (P > 1) {
+            // stacked: the own block at columns [pi R, pi R + R), zeros in the other blocks
+            uint8_t* lt = smem + L.al;
+#pragma unroll
+            for (int c8 = 0; c8 < 16; ++c8) {
+                const int col = c8 * 8;
+                if (col < pi * R || col >= pi * R + R)
+                    *reinterpret_cast<uint4*>(lt + (col >> 6) * L.panel + sw128_offset(t, col & 63)) =
+                        make_uint4(0u, 0u, 0u, 0u);
+            }
+#pragma unroll
+            for (int c8 = 0; c8 < NCH * 4; ++c8) {
+                uint32_t w[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const uint64_t q2 = FINAL ? s2[4 * c8 + e] : fmul2(s2[4 * c8 + e], inv2);
+                    w[e] = pack_bf16(lo2(q2), hi2(q2));
+                }
+                const int col = pi * R + c8 * 8;
+                *reinterpret_cast<uint4*>(lt + (col >> 6) * L.panel + sw128_offset(t, col & 63)) =
+                    make_uint4(w[0], w[1], w[2], w[3]);
+            }
+        } else if (t < R) {
             uint8_t* lt = smem + L.al;
 #pragma unroll
             for (int c8 = 0; c8 < NCH * 4; ++c8) {
@@ -313,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : 4) lstep_tc_kernel(co
     tc_fence_after();
     TRACEL(3);
 
-    const uint32_t nk = (uint32_t)R / 16;
+    const uint32_t nk = (uint32_t)RT / 16;
     if (!FINAL) {
         // cR[k,i] = sum_j L[j,k]  (monarch.hpp:139-143) on the tensor core: L^T 1 with
         // A = L^T (M=k, K=j) MN-major, B = 16 columns of ones, into TMEM columns [0, 16); read
@@ -329,11 +377,11 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : 4) lstep_tc_kernel(co
         __syncwarp();
         mbar_wait(bar_cr, 0);
         tc_fence_after();
-        if (warp * 32 < m) {
+        if (warp * 32 < (P == 1 ? m : RT)) {
             uint32_t v;
             asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(tmem + lane_base));
             tmem_ld_wait();
-            if (t < m) a.cR[((int64_t)u * m + t) * a.b + i] = __uint_as_float(v);
+            if (row_ok) a.cR[((int64_t)u * m + rr) * a.b + i + pi] = __uint_as_float(v);
         }
         tc_fence_before();
         __syncthreads();
@@ -371,11 +419,11 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : 4) lstep_tc_kernel(co
     const float scale = FINAL ? a.out_scale * inv_row : a.out_scale;
 #pragma unroll
     for (int cc = 0; cc < 4; ++cc) {
-        if (warp * 32 >= R) break;  // no output row in this warp
+        if (warp * 32 >= RT) break;  // no output row in this warp
         uint32_t orr[32];
         VMB_TMEM_LD32(tmem + lane_base + cc * 32, orr);
         tmem_ld_wait();
-        if (t < R) {
+        if (t < RT) {
             uint8_t* panel = smem + L.qb + (cc >> 1) * L.panel;
 #pragma unroll
             for (int x = 0; x < 4; ++x) {
@@ -393,13 +441,13 @@ __global__ void __launch_bounds__(kThreads, NCH == 4 ? 2 : 4) lstep_tc_kernel(co
     __syncthreads();
     TRACEL(6);
     if (t == 0) {
-        if (!FINAL) {
-            tma_store_5d(&a.tmOut, smem + L.qb, 0, i, 0, 0, u);
-            tma_store_5d(&a.tmOut, smem + L.qb + L.panel, 64, i, 0, 0, u);
-        } else {
-            const int ob = u / a.oHn, oh = u % a.oHn;
-            tma_store_5d(&a.tmOut, smem + L.qb, 0, i, 0, oh, ob);
-            tma_store_5d(&a.tmOut, smem + L.qb + L.panel, 64, i, 0, oh, ob);
+        // one store box per position (a position past b is clipped by the map)
+        const int ob = FINAL ? u / a.oHn : u, oh = FINAL ? u % a.oHn : 0;
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            const uint32_t o = (uint32_t)(q * R) * 128u;
+            tma_store_5d(&a.tmOut, smem + L.qb + o, 0, i + q, 0, oh, ob);
+            tma_store_5d(&a.tmOut, smem + L.qb + L.panel + o, 64, i + q, 0, oh, ob);
         }
         tma_store_commit();
         tma_store_wait_read();
@@ -688,13 +736,13 @@ void launch_hl(const HlParams& p, int64_t U, cudaStream_t s) {
     }
 }
 
-template <bool FINAL, int NCH>
+template <bool FINAL, int NCH, int P>
 void launch_nch(const Params& p, int64_t U, cudaStream_t s) {
-    const Layout L(p.rows, FINAL);
+    const Layout L(P * p.rows, FINAL);
     const int smem = (int)L.bytes + 1024;
-    auto kern = lstep_tc_kernel<FINAL, NCH>;
+    auto kern = lstep_tc_kernel<FINAL, NCH, P>;
     VMB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    dim3 grid((unsigned)p.a.b, (unsigned)U);
+    dim3 grid((unsigned)((p.a.b + P - 1) / P), (unsigned)U);
     ProfScope ps(FINAL ? kKLfinal : kKLstep, s);
     kern<<<grid, kThreads, smem, s>>>(p);
     count_launch();
@@ -703,11 +751,16 @@ void launch_nch(const Params& p, int64_t U, cudaStream_t s) {
 
 template <bool FINAL>
 void launch(const Params& p, int64_t U, cudaStream_t s) {
+    switch (lstep_positions(p.a.m)) {
+        case 4: launch_nch<FINAL, 1, 4>(p, U, s); return;  // rows per position 32
+        case 2: launch_nch<FINAL, 2, 2>(p, U, s); return;  // 64
+        default: break;
+    }
     switch ((p.rows + 31) / 32) {
-        case 1: launch_nch<FINAL, 1>(p, U, s); break;
-        case 2: launch_nch<FINAL, 2>(p, U, s); break;
-        case 3: launch_nch<FINAL, 3>(p, U, s); break;
-        default: launch_nch<FINAL, 4>(p, U, s); break;
+        case 1: launch_nch<FINAL, 1, 1>(p, U, s); break;
+        case 2: launch_nch<FINAL, 2, 1>(p, U, s); break;
+        case 3: launch_nch<FINAL, 3, 1>(p, U, s); break;
+        default: launch_nch<FINAL, 4, 1>(p, U, s); break;
     }
 }
 
@@ -739,7 +792,7 @@ void tc_lstep_launch(const TcLstepArgs& a, int64_t U, cudaStream_t s) {
     VMB_REQUIRE_DIM(a.b <= 2147483647 && U <= 65535, "tcgen05 L-step grid limits");
     Params p;
     p.a = a;
-    p.rows = lstep_rows(a.m);
+    p.rows = lstep_box_rows(a.m);
     if (a.final_mode) launch<true>(p, U, s);
     else launch<false>(p, U, s);
 }

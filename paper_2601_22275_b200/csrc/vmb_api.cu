@@ -433,7 +433,7 @@ void forward(const Shape& s, const vmb_config& cfg, vmb_dtype dt, const void* q,
         const CUtensorMap mV = user_map(v, kin, s, b, 1, m, b, 128, 1);
         const CUtensorMap mK2 = user_map(k, kin, s, b, 1, m, b, kRstepKvBox, 1);  // fa2: 64-key tiles
         // (the lstep_tc boxes; with m > 128 the multi-pass L-step builds its own maps)
-        const uint32_t lrows = (uint32_t)std::min<int64_t>(lstep_rows(m), 128);
+        const uint32_t lrows = (uint32_t)std::min<int64_t>(lstep_box_rows(m), 128);
         const CUtensorMap mQcol = user_map(q, in, s, bq, 1, m, bq, 1, lrows);   // (d, i, j): Qb[i] boxes
         const CUtensorMap mAR = internal_map(ws.aR, U, m, bq, d, true, 128, 1);  // aR (U,m,bq,d): (d,i,k) query tiles
         const CUtensorMap mARst = internal_map(ws.aR, U, m, bq, d, true, 1, lrows);  // aR columns (d,i,k), L-step store
@@ -1400,7 +1400,7 @@ vmb_status vmb_lstep(int64_t units, int64_t m, int64_t b, int64_t d, vmb_dtype d
         }
         if (tc) {
             TcLstepArgs ls{};
-            const uint32_t lrows = (uint32_t)lstep_rows(m);
+            const uint32_t lrows = (uint32_t)lstep_box_rows(m);
             // Qb (U, b, m, d): rows (u, i, j); map dims (d, i, j, 1, U)
             {
                 const uint64_t dims[5] = {(uint64_t)d, (uint64_t)b, (uint64_t)m, 1, (uint64_t)std::max<int64_t>(units, 1)};

@@ -68,6 +68,8 @@ BF16_CASES = [
     ((21, 6, 7), 1, 1, 1.0, dict()),                 # m = 21 (Wan temporal size), b = 42
     ((81, 3, 4), 1, 1, 1.0, dict()),                 # m = 81 (321-frame temporal size)
     ((100, 2, 3), 1, 1, 1.0, dict()),                # m = 100 > 96: L-step column sums on the tensor core
+    ((49, 3, 5), 2, 1, 1.0, dict()),                 # m = 49: two positions per L-step CTA, b = 15 odd
+    ((21, 5, 3), 1, 1, 2.0, dict(iters=3)),          # m = 21: four positions per L-step CTA, b = 15
     ((6, 9, 11), 2, 1, 3.0, dict()),                 # peaky attention, sigma 3
     ((4, 8, 16), 1, 1, 2.0, dict(iters=1)),
     ((4, 8, 16), 1, 1, 2.0, dict(clamp_min=0.9)),    # clamp-forcing
@@ -114,8 +116,9 @@ def test_rstep_parity(vm, orc, cuda, dtype, tol, m, b, d):
 
 
 @pytest.mark.parametrize("dtype,tol", [(torch.float32, 1e-5), (torch.bfloat16, BF16_TOL)])
-@pytest.mark.parametrize("m,b,d", [(4, 16, 128), (21, 40, 128), (81, 8, 128), (96, 5, 128), (100, 4, 128),
-                                   (128, 3, 128), (5, 7, 32)])
+@pytest.mark.parametrize("m,b,d", [(4, 16, 128), (21, 40, 128), (21, 7, 128), (33, 6, 128), (49, 5, 128),
+                                   (64, 3, 128), (81, 8, 128), (96, 5, 128), (100, 4, 128), (128, 3, 128),
+                                   (5, 7, 32)])
 def test_lstep_parity(vm, orc, cuda, dtype, tol, m, b, d):
     rng = np.random.default_rng(2)
     Qb = bf16_round(rng.standard_normal((2, b, m, d)).astype(np.float32) / np.sqrt(d))
