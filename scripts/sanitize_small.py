@@ -16,6 +16,11 @@ r = lambda *s: torch.randn(*s, generator=g, device=dev).to(torch.bfloat16)  # no
 grid = vm.TokenGrid(3, 10, 20, 128, 2, 1)
 q, k, v = r(2, grid.tokens(), 128), r(2, grid.tokens(), 128), r(2, grid.tokens(), 128)
 vm.vmonarch_attention(q, k, v, grid)
+# L-step with two positions per CTA (m = 49, ragged b = 15) and one position (m = 81)
+for tg in ((49, 3, 5), (81, 3, 4)):
+    gg = vm.TokenGrid(*tg, 128, 1, 1)
+    z = r(1, gg.tokens(), 128)
+    vm.vmonarch_attention(z, z, z, gg)
 # m > 128 (lstep_big), d < 128 (padding)
 g2 = vm.TokenGrid(8, 8, 8, 128, 1, 1)
 x = r(1, g2.tokens(), 128)
