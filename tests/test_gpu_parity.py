@@ -116,7 +116,7 @@ def test_rstep_parity(vm, orc, cuda, dtype, tol, m, b, d):
 
 
 @pytest.mark.parametrize("dtype,tol", [(torch.float32, 1e-5), (torch.bfloat16, BF16_TOL)])
-@pytest.mark.parametrize("m,b,d", [(4, 16, 128), (21, 40, 128), (21, 7, 128), (33, 6, 128), (49, 5, 128),
+@pytest.mark.parametrize("m,b,d", [(4, 16, 128), (5, 2, 128), (21, 40, 128), (21, 7, 128), (33, 6, 128), (49, 5, 128),
                                    (64, 3, 128), (81, 8, 128), (96, 5, 128), (100, 4, 128), (128, 3, 128),
                                    (5, 7, 32)])
 def test_lstep_parity(vm, orc, cuda, dtype, tol, m, b, d):
